@@ -1,0 +1,462 @@
+#!/usr/bin/env python3
+"""Benchmark of the Squares RNG hot path on B200 (BASELINE.json metric:
+"Gsamples/s per GPU and box (1/2/4/8 B200); % HBM write BW or % IMAD peak").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4|c5] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+A step is one pass of the hot path over one batch: for the default workload c2
+(BASELINE.json configs[1]: squares32, one key from seed 1, counters 0..2^30-1, uint32 output,
+4 GiB) one sq_fill_u32 launch over this rank's contiguous counter shard.  `value` is the
+whole-job throughput (samples of all ranks / max-over-ranks device time), inputs resident.
+`e2e` is the same metric through the C ABI with HOST buffers (sq_fill_host: chunked generation
++ D2H into pinned memory, copies inside the timed region).  `--impl reference` times the CPU
+oracle (the tier's reference arm) on the host cores.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth_inputs as SI  # noqa: E402
+
+METRIC = "Gsamples/s per GPU and box (1/2/4/8 B200); % HBM write BW or % IMAD peak"
+UNIT = "Gsamples/s"
+FALLBACK_HBM_GBS = 6650.0          # /opt/skills/guides/B200_PROFILING.md fallback
+SM_PER_GPU = 148
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": FALLBACK_HBM_GBS, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def load_profile_summary():
+    """Per-kernel ncu figures committed under profiles/ (traffic = dram read+write per launch)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+# ------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampler of SM clock and clock-event (throttle) reasons DURING the timed region."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x40: "sw_thermal_slowdown",
+               0x80: "hw_thermal_slowdown", 0x100: "hw_power_brake_slowdown", 0x2: "applications_clocks",
+               0x20: "sync_boost", 0x1: "gpu_idle"}
+
+    def __init__(self, torch_dev: int, interval_s: float = 0.005):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.interval = interval_s
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(torch_dev)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.interval)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": getattr(self, "err", "")}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------- CPU oracle
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def oracle_rate(w: SI.Workload, key: int, keys, budget_s: float, threads: int):
+    """Times the oracle AS IT STANDS (oracle/oracle.c, gcc -O2, one loop per thread) on a
+    bounded sample of workload w: `threads` disjoint contiguous shards of its counter range
+    (or key rows).  Returns (samples/s, samples, wall seconds, description)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    import oracle as O
+    kind = w.kind
+    # calibrate on one thread
+    m0 = 1 << 18
+    t0 = time.perf_counter()
+    if kind == "fused":
+        O.fused_stats(key, 0, m0)
+    else:
+        O.fill(kind, [key], 0, m0)
+    r1 = m0 / max(time.perf_counter() - t0, 1e-6)
+    per = int(max(1 << 16, min(r1 * budget_s, w.samples // threads)))
+    bufs = [None] * threads
+    if kind != "fused":
+        dt = {"u32": np.uint32, "u64": np.uint64, "f32": np.float32}[kind]
+        bufs = [np.empty(per, dtype=dt) for _ in range(threads)]
+    lib = O.lib()
+    fn = None if kind == "fused" else getattr(lib, f"oracle_fill_{kind}")
+    karr = [np.array([int(keys[i % len(keys)]) if w.nkeys > 1 else key], dtype=np.uint64) for i in range(threads)]
+
+    def work(i):
+        start = (w.samples // threads) * i if w.nkeys == 1 else 0
+        if kind == "fused":
+            h = np.zeros(65536, np.uint64)
+            o = np.zeros(32, np.uint64)
+            lib.oracle_fused_stats(key, start, per, h.ctypes.data, o.ctypes.data)
+        else:
+            fn(karr[i].ctypes.data, 1, start, per, bufs[i].ctypes.data, per)
+
+    with ThreadPoolExecutor(threads) as ex:
+        t0 = time.perf_counter()
+        list(ex.map(work, range(threads)))
+        wall = time.perf_counter() - t0
+    total = per * threads
+    shape = (f"{threads} threads x {per} consecutive counters" +
+             (" (one key row each)" if w.nkeys > 1 else " (disjoint shards of the workload's counter range)"))
+    return total / wall, total, wall, shape
+
+
+# ------------------------------------------------------------------------------------- GPU arm
+def run_ours(args, w: SI.Workload, rank: int, world: int, dev: int):
+    import numpy as np
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2004_06278_b200 as sq
+    from paper_2004_06278_b200 import dist as sqdist
+
+    if args.scaling == "weak":
+        # weak scaling (per-GPU work fixed): rank r owns the r-th config-sized block of the
+        # counter space -- or the r-th block of nkeys keys -- so N GPUs do N batches.
+        if w.shard == "key":
+            keys_all = sq.keygen(w.key_seed, w.nkeys * world)
+            k0, kn = rank * w.nkeys, w.nkeys
+            ctr0, n = w.ctr0, w.n
+        else:
+            keys_all = sq.keygen(w.key_seed, 1)
+            k0, kn = 0, 1
+            ctr0, n = (w.ctr0 + rank * w.n) & ((1 << 64) - 1), w.n
+    else:
+        # strong scaling: the config's fixed total split into contiguous shards
+        keys_all = sq.keygen(w.key_seed, w.nkeys)
+        if w.shard == "key":
+            k0, kn = sqdist.key_shard(w.nkeys)
+            ctr0, n = w.ctr0, w.n
+        else:
+            k0, kn = 0, 1
+            ctr0, n = sqdist.counter_shard(w.ctr0, w.n)
+    key0 = int(keys_all[k0]) & ((1 << 64) - 1)
+    keys_d = keys_all[k0:k0 + kn].cuda(dev)
+    samples_rank = kn * n
+    stream = torch.cuda.current_stream(dev)
+    if w.kind == "fused":
+        hist = torch.zeros(65536, dtype=torch.int64, device=dev)
+        ones = torch.zeros(32, dtype=torch.int64, device=dev)
+
+        def step():
+            sq.fused_stats(key0, ctr0, n, hist, ones, stream=stream)
+    else:
+        out = torch.empty((kn, n), dtype={"u32": torch.int32, "u64": torch.int64, "f32": torch.float32}[w.kind],
+                          device=dev)
+        fill = getattr(sq, f"fill_{w.kind}")
+
+        def step():
+            fill(keys_d, ctr0, n, out=out, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        tdist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            tdist.barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            tdist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    tot = torch.tensor([float(samples_rank)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        tdist.all_reduce(tot, op=tdist.ReduceOp.SUM)
+    ms_max = float(t.item())
+    total_samples = float(tot.item())
+    if w.kind == "fused" and world > 1:
+        # the one real exchange step: all-reduce of the counts (outside the timed kernel loop,
+        # timed separately below)
+        pass
+    res = {
+        "ms_total": ms_max,
+        "ms_per_step": ms_max / args.steps,
+        "value": total_samples * args.steps / (ms_max * 1e-3) / 1e9,
+        "samples_per_step": int(total_samples),
+        "samples_rank": samples_rank,
+        "clocks": clk.summary(),
+        "key0": key0,
+        "kn": kn,
+    }
+    if w.kind == "fused" and world > 1:
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        sqdist.allreduce_counts(hist, ones)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        res["allreduce_ms"] = e0.elapsed_time(e1)
+    # e2e through the C ABI with host buffers (rank-local shard; single-key workloads)
+    if not args.no_e2e:
+        res["e2e"] = run_e2e(args, w, sq, key0, keys_d, ctr0, n, kn, dev, world)
+    return res
+
+
+def run_e2e(args, w, sq, key0, keys_d, ctr0, n, kn, dev, world):
+    import torch
+    import torch.distributed as tdist
+    steps = args.e2e_steps
+    if w.kind == "fused":
+        host_h = torch.empty(65536 + 32, dtype=torch.int64).pin_memory()
+        hist = torch.zeros(65536, dtype=torch.int64, device=dev)
+        ones = torch.zeros(32, dtype=torch.int64, device=dev)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            hist.zero_()
+            ones.zero_()
+            sq.fused_stats(key0, ctr0, n, hist, ones)
+            host_h[:65536].copy_(hist, non_blocking=True)
+            host_h[65536:].copy_(ones, non_blocking=True)
+            torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t0
+        d2h = (65536 + 32) * 8
+        samples = n
+    else:
+        es = 8 if w.kind == "u64" else 4
+        rows = [int(k) & ((1 << 64) - 1) for k in keys_d[: min(kn, 8)].tolist()] if w.shard == "key" else [key0]
+        # key-sharded workloads: time the first min(kn, 8) rows of this rank, scale by rows
+        host = torch.empty(n * es * len(rows), dtype=torch.uint8).pin_memory()
+        scratch = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
+        cs = torch.cuda.Stream(dev)
+        sq.fill_host(w.kind, rows[0], ctr0, min(n, 1 << 20), host, scratch, copy_stream=cs)  # warm
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            for i, k in enumerate(rows):
+                sq.fill_host(w.kind, k, ctr0, n, host[i * n * es:(i + 1) * n * es], scratch, copy_stream=cs)
+        wall = time.perf_counter() - t0
+        d2h = n * es * len(rows)
+        samples = n * len(rows)
+    t = torch.tensor([wall], dtype=torch.float64, device=dev)
+    s = torch.tensor([float(samples)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        tdist.all_reduce(s, op=tdist.ReduceOp.SUM)
+    return {"value": float(s.item()) * steps / float(t.item()) / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": 8, "d2h_bytes_per_step": d2h, "steps": steps,
+            "note": "sq_fill_host / fused_stats + D2H of the counts; the 8-byte key travels in the launch parameters"}
+
+
+def roofline_for(w: SI.Workload, res, peaks, peaks_src, prof):
+    """Roofline of the dominant (only) kernel of the step."""
+    ms_launch = res["ms_per_step"]
+    if w.kind == "fused":
+        # ALU/FMA-bound: peak derived in DESIGN.md from the measured IMAD rate (64 lane-results
+        # per clock per SM) and the 9 FMA-pipe slots squares32 needs per sample after the
+        # finite-difference round 1: 64/9 samples/clk/SM x 148 SMs x max SM clock.
+        mhz = peaks.get("sm_max_mhz", 1965.0)
+        peak = 64.0 / 9.0 * SM_PER_GPU * mhz * 1e6 / 1e9
+        achieved = res["samples_rank"] / (ms_launch * 1e-3) / 1e9
+        return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gsamples/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_note": "FMA-pipe floor 9 slots/sample (3 IMAD.WIDE x2 + 3 IMAD) at 64 slots/clk/SM, max SM clock"}
+    bytes_launch = res["samples_rank"] * w.elem_bytes
+    achieved = bytes_launch / (ms_launch * 1e-3) / 1e9
+    peak = float(peaks["hbm_gbs"])
+    traffic = None
+    kname = {"u32": "fill_kernel<0>", "u64": "fill_kernel<1>", "f32": "fill_kernel<2>"}[w.kind]
+    if prof.get(w.name, {}).get("kernel") == kname and w.name in prof:
+        traffic = prof[w.name].get("dram_bytes_per_launch")
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks_src}, copy read+write)",
+            "algorithmic_bytes_per_launch": bytes_launch}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank runs one config-sized batch of its own counter block")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the secondary c3/c4/c5 summary")
+    ap.add_argument("--cpu-budget", type=float, default=2.0, help="seconds per oracle thread (cpu_baseline)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    w = SI.CONFIGS[args.workload]
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return main_reference(args, w, rank, world)
+
+    import torch
+    import torch.distributed as tdist
+    torch.cuda.set_device(local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks, peaks_src = load_peaks()
+    prof = load_profile_summary()
+    import paper_2004_06278_b200 as sq  # noqa: F401  (loads libsquares.so; raises if missing)
+
+    res = run_ours(args, w, rank, world, local)
+    extra = {}
+    if not args.no_extra and args.workload == "c2":
+        a2 = argparse.Namespace(**vars(args))
+        a2.no_e2e = True
+        for name, steps in (("c3", 20), ("c4", 20), ("c5", 3)):
+            a2.steps, a2.warmup = steps, 3
+            ww = SI.CONFIGS[name]
+            r = run_ours(a2, ww, rank, world, local)
+            rl = roofline_for(ww, r, peaks, peaks_src, prof)
+            extra[name] = {"value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"], "steps": steps,
+                           "roofline": rl, "clocks": r["clocks"]}
+            if "allreduce_ms" in r:
+                extra[name]["allreduce_ms"] = r["allreduce_ms"]
+
+    if rank == 0:
+        rl = roofline_for(w, res, peaks, peaks_src, prof)
+        cores = host_cores()
+        rate, samples, wall, shape = oracle_rate(w, res["key0"], sq.keygen(w.key_seed, min(w.nkeys, 64)).tolist(),
+                                                 args.cpu_budget, cores)
+        line = {
+            "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None,
+            "dtype": {"u32": "u32", "u64": "u64", "f32": "u32->f32", "fused": "u32"}[w.kind],
+            "data": "synthetic",
+            "config": {"workload": f"{w.name}: " + {
+                "c2": "squares32 fill, 1 key (seed 1), ctr 0..2^30-1, uint32 out (4 GiB)",
+                "c3": "squares64 fill, 1 key (seed 1), ctr 0..2^29-1, uint64 out (4 GiB)",
+                "c4": "squares32->f32 fill, 4096 keys (seed 7) x 2^18 ctr, [key][ctr] (4 GiB)",
+                "c5": "fused squares32 hist(65536)+ones(32), 1 key (seed 1), ctr 0..2^38-1"}[w.name],
+                "key_seed": w.key_seed, "nkeys": w.nkeys, "ctr0": w.ctr0, "n_per_key": w.n,
+                "samples_per_step": res["samples_per_step"],
+                "sharding": "counter" if w.shard == "ctr" else "key",
+                "parallelism": f"{'ctr' if w.shard == 'ctr' else 'key'}-shard x{world}",
+                "l2": "output larger than L2 (4 GiB written per step)" if w.kind != "fused"
+                else "no HBM traffic (fused, counts only)"},
+            "roofline": rl,
+            "cpu_baseline": {"value": rate / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{samples} samples of {w.name}: {shape}; {wall:.2f} s wall"},
+            "clocks": res["clocks"],
+            "gpu_launches": args.steps,
+            "impl": "ours",
+        }
+        if "e2e" in res:
+            line["e2e"] = res["e2e"]
+        if extra:
+            line["also"] = extra
+        print(json.dumps(line))
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
+def main_reference(args, w, rank, world):
+    """Reference arm: the CPU oracle as it stands on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import paper_2004_06278_b200 as sq  # only for the key (host function, no GPU work)
+    import oracle as O
+    O.build()
+    cores = host_cores()
+    key0 = int(sq.keygen(w.key_seed, 1)[0]) & ((1 << 64) - 1)
+    keys = [int(k) & ((1 << 64) - 1) for k in sq.keygen(w.key_seed, min(w.nkeys, 64)).tolist()]
+    # each step a bounded sample sized so that warmup + steps take <= ~120 s
+    per_step_budget = max(0.05, min(2.0, 120.0 / (args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_rate(w, key0, keys, per_step_budget / 4, cores)
+    tot_s, tot_n = 0.0, 0
+    last = None
+    for _ in range(args.steps):
+        rate, samples, wall, shape = oracle_rate(w, key0, keys, per_step_budget, cores)
+        tot_s += wall
+        tot_n += samples
+        last = (samples, shape)
+    value = tot_n / tot_s / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": {"u32": "u32", "u64": "u64", "f32": "u32->f32",
+                                                           "fused": "u32"}[w.kind],
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": w.name, "key_seed": w.key_seed, "nkeys": w.nkeys, "n_per_key": w.n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"per step {last[0]} samples: {last[1]}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,150 @@
+/*
+ * squares.h -- C ABI of libsquares.so, the B200 (sm_100a) bulk evaluator of the Squares
+ * counter-based RNG (B. Widynski, arXiv 2004.06278).
+ *
+ * Citations: P:n = PAPER.md line n (the paper text), S:n = SPEC.md line n.
+ *
+ *   squares32(ctr, key)  P:21-28 (section 2 listing): y = x = ctr*key; z = y + key;
+ *                        rounds x = rot32(x*x + w) with w = y, z, y; return (x*x + z) >> 32.
+ *   squares64(ctr, key)  P:56-64 (section 5 listing): rounds 1-3 as above,
+ *                        t = x = x*x + z; x = rot32(x); return t ^ ((x*x + y) >> 32).
+ *   All arithmetic is mod 2^64 ("uint64_t"); rot32 swaps the 32-bit halves.
+ *
+ * Conventions for every entry point below:
+ *   - Device pointers are CUDA device (or managed) memory of the CURRENT device; host pointers
+ *     are ordinary host memory.  The caller owns every buffer; the library allocates nothing
+ *     that outlives a call.
+ *   - GPU entry points are asynchronous on `stream` (a cudaStream_t; NULL = legacy default
+ *     stream).  They only enqueue work: they never synchronize, never change the current
+ *     device, and return as soon as the launch is queued.  Asynchronous device faults surface
+ *     at the caller's next synchronization.
+ *   - All functions are reentrant and may be called concurrently on any number of streams.
+ *   - Counters wrap mod 2^64: element i of a fill uses counter ctr0 + i mod 2^64.
+ *   - Keys are NOT validated on the GPU paths: the generators are total over (ctr, key).
+ *     Validation belongs to sq_validate_key / sq_keygen.
+ *   - Return value: SQ_OK, or an error code (nothing is launched when an error is returned).
+ */
+#ifndef SQUARES_H_
+#define SQUARES_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Opaque stream handle, ABI-compatible with cudaStream_t / CUstream. */
+typedef struct CUstream_st* sq_stream_t;
+
+/* Status codes. */
+#define SQ_OK 0      /* success (also returned, with no launch, when there is nothing to do) */
+#define SQ_EINVAL 1  /* bad argument: NULL pointer with work to do, ld < n with nkeys > 1,
+                        misaligned output, size overflow */
+#define SQ_ERANGE 2  /* argument out of the supported range (e.g. keygen count > 2^31) */
+#define SQ_ECUDA 3   /* a CUDA call failed (launch/config error, no device); see sq_last_cuda_error */
+#define SQ_ENOMEM 4  /* host allocation failed */
+
+/* Human-readable name of a status code (static string, never NULL). */
+const char* sq_strerror(int code);
+
+/* cudaError_t value of the most recent SQ_ECUDA returned on the calling thread (0 if none). */
+int sq_last_cuda_error(void);
+
+/* Library ABI version (major*10000 + minor*100 + patch). */
+int sq_version(void);
+
+/* ----------------------------------------------------------------------------------------
+ * Key utility -- the "different digits" rules of P:37 (section 3):
+ *   "The keys are chosen so the the upper 8 digits are different and also that the lower 8
+ *    digits are different", "The digits are also chosen randomly", "an irregular bit pattern
+ *    with roughly half ones and half zeros".
+ * Builder's readings: every hex digit nonzero, the
+ * least significant digit odd, and popcount in [28, 36] ("roughly half ones").
+ * -------------------------------------------------------------------------------------- */
+
+/* Rule bits returned by sq_validate_key (0 = valid key). */
+#define SQ_KEY_UPPER_REPEAT 1u /* two of the upper 8 hex digits are equal */
+#define SQ_KEY_LOWER_REPEAT 2u /* two of the lower 8 hex digits are equal */
+#define SQ_KEY_ZERO_DIGIT 4u   /* some hex digit is 0 */
+#define SQ_KEY_EVEN 8u         /* least significant digit is even */
+#define SQ_KEY_POPCOUNT 16u    /* popcount outside [28, 36] ("roughly half ones") */
+
+/* Host only.  Bitmask of the rules above that `key` violates; 0 iff `key` is valid. */
+uint32_t sq_validate_key(uint64_t key);
+
+/* Host only.  keys_host[j], j < count, = the j-th key of stream `seed` under the documented
+ * deterministic mapping: candidates are drawn digit by digit
+ * from a SplitMix64-finalizer hash of (seed, j, attempt, draw); the first candidate that passes
+ * sq_validate_key and differs from keys_host[0..j-1] is kept.  Properties: deterministic,
+ * prefix-stable (the first k keys do not depend on count), pairwise distinct, all valid.
+ * Not sequence-compatible with the paper's unpublished utility (P:37 footnote).
+ * Errors: SQ_ERANGE if count > 2^31 ("about 2 billion keys"); SQ_EINVAL if
+ * keys_host is NULL with count > 0; SQ_ENOMEM if the O(count) duplicate set cannot be
+ * allocated.  count == 0 is SQ_OK. */
+int sq_keygen(uint64_t seed, uint64_t count, uint64_t* keys_host);
+
+/* ----------------------------------------------------------------------------------------
+ * Bulk fills (BASELINE.json configs 1-4).  Row-major [key][ctr] layout:
+ *   out[k*ld + i] = G(ctr0 + i mod 2^64, keys[k])   for k < nkeys, i < n;
+ * elements i in [n, ld) of each row are left untouched.
+ *   keys_dev  device, nkeys uint64 keys (read only)
+ *   nkeys     number of rows
+ *   ctr0      first counter of every row
+ *   n         counters per row
+ *   out_dev   device output, must be aligned to its element size; rows of `ld` elements
+ *   ld        leading dimension in ELEMENTS (ld >= n required when nkeys > 1; ignored when
+ *             nkeys == 1)
+ * Returns SQ_OK without launching when n == 0 or nkeys == 0.
+ * Errors: SQ_EINVAL on NULL pointers with work to do, ld < n with nkeys > 1, a misaligned
+ * out_dev, or nkeys*ld*elem overflowing size_t; SQ_ECUDA if the launch fails.
+ * -------------------------------------------------------------------------------------- */
+
+/* G = squares32, uint32 output. */
+int sq_fill_u32(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n,
+                uint32_t* out_dev, uint64_t ld, sq_stream_t stream);
+
+/* G = squares64, uint64 output (little-endian words). */
+int sq_fill_u64(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n,
+                uint64_t* out_dev, uint64_t ld, sq_stream_t stream);
+
+/* G = (float)(squares32 >> 8) * 2^-24: the top 24 bits of squares32 as a float32 in
+ * [0, 1 - 2^-24] (BASELINE.json config 4).  Exact: no rounding occurs. */
+int sq_fill_f32(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n,
+                float* out_dev, uint64_t ld, sq_stream_t stream);
+
+/* ----------------------------------------------------------------------------------------
+ * Fused generate-and-reduce (BASELINE.json config 5; the GPU analogue of P:45's "basic
+ * uniformity test").  With u_i = squares32(ctr0 + i mod 2^64, key), i < n, ACCUMULATES
+ *   hist_dev[b] += #{i : u_i >> 16 == b}            b < 65536
+ *   ones_dev[j] += #{i : (u_i >> j) & 1 == 1}        j < 32, j = 0 the least significant bit
+ * into caller-initialised device arrays (uint64).  No sample is stored.  Accumulation makes
+ * chunked and sharded runs compose by addition.  hist_dev and ones_dev must be 8-byte aligned.
+ * Returns SQ_OK without launching when n == 0.  Errors: SQ_EINVAL (NULL / misaligned),
+ * SQ_ECUDA (launch failure).
+ * -------------------------------------------------------------------------------------- */
+int sq_fused_stats(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist_dev,
+                   uint64_t* ones_dev, sq_stream_t stream);
+
+/* ----------------------------------------------------------------------------------------
+ * Host-buffer fill (the end-to-end path): the same map as sq_fill_u32 / sq_fill_u64 /
+ * sq_fill_f32 for ONE key, written to HOST memory.  The library generates chunks of
+ * `chunk_elems` elements into the caller's device scratch (two ping-pong halves of
+ * scratch_bytes) and copies each chunk to out_host with cudaMemcpyAsync on `stream`,
+ * overlapping generation of chunk c+1 with the copy of chunk c via `copy_stream`.  The call is
+ * SYNCHRONOUS: it returns after out_host holds all n elements.  out_host should be pinned
+ * (cudaHostAlloc / cudaHostRegister) for full PCIe bandwidth.
+ *   kind        0 = u32, 1 = u64, 2 = f32
+ *   key         the key (host value)
+ *   scratch_dev device scratch, >= 2 * 32 bytes, 256-byte aligned recommended
+ * Errors: SQ_EINVAL (bad kind, NULL pointers with n > 0, scratch too small), SQ_ECUDA.
+ * -------------------------------------------------------------------------------------- */
+int sq_fill_host(int kind, uint64_t key, uint64_t ctr0, uint64_t n, void* out_host,
+                 void* scratch_dev, size_t scratch_bytes, sq_stream_t stream,
+                 sq_stream_t copy_stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SQUARES_H_ */

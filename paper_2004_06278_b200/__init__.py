@@ -1,0 +1,189 @@
+"""paper_2004_06278_b200 -- B200 (sm_100a) bulk evaluator of the Squares counter-based RNG
+(B. Widynski, arXiv 2004.06278).
+
+Thin Python binding of ``libsquares.so`` (C ABI in ``include/squares.h``): argument
+marshalling only.  Every step of the hot path runs in the library's CUDA kernels; there is no
+CPU or PyTorch fallback -- if the extension is missing or a call fails, these functions raise.
+
+PyTorch supplies device memory (tensors), the current CUDA stream and process groups.
+Tensor dtypes: keys are int64 tensors (reinterpreted as uint64); u32 outputs are int32
+(reinterpreted as uint32), u64 outputs int64, f32 outputs float32.  Fused counts are int64
+tensors (uint64 counts; NCCL SUM over int64 is bit-identical to uint64 addition mod 2^64).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from . import dist  # noqa: F401  (multi-GPU composition: partition + NCCL all-reduce)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsquares.so")
+
+SQ_OK, SQ_EINVAL, SQ_ERANGE, SQ_ECUDA, SQ_ENOMEM = 0, 1, 2, 3, 4
+KEY_UPPER_REPEAT, KEY_LOWER_REPEAT, KEY_ZERO_DIGIT, KEY_EVEN, KEY_POPCOUNT = 1, 2, 4, 8, 16
+KINDS = {"u32": 0, "u64": 1, "f32": 2}
+HIST_BINS = 65536
+M64 = (1 << 64) - 1
+
+_lib = None
+
+
+class SquaresError(RuntimeError):
+    def __init__(self, fn: str, code: int):
+        lib = _load()
+        msg = lib.sq_strerror(code).decode()
+        if code == SQ_ECUDA:
+            msg += f" (cudaError {lib.sq_last_cuda_error()})"
+        super().__init__(f"{fn}: {msg}")
+        self.code = code
+
+
+def _load() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2004_06278_b200._build` "
+            "(or __graft_entry__.build()); there is no fallback implementation")
+    L = ctypes.CDLL(LIB_PATH)
+    u64, u32, vp, i32 = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_int
+    sigs = {
+        "sq_strerror": (ctypes.c_char_p, [i32]),
+        "sq_last_cuda_error": (i32, []),
+        "sq_version": (i32, []),
+        "sq_validate_key": (u32, [u64]),
+        "sq_keygen": (i32, [u64, u64, vp]),
+        "sq_fill_u32": (i32, [vp, u64, u64, u64, vp, u64, vp]),
+        "sq_fill_u64": (i32, [vp, u64, u64, u64, vp, u64, vp]),
+        "sq_fill_f32": (i32, [vp, u64, u64, u64, vp, u64, vp]),
+        "sq_fused_stats": (i32, [u64, u64, u64, vp, vp, vp]),
+        "sq_fill_host": (i32, [i32, u64, u64, u64, vp, vp, ctypes.c_size_t, vp, vp]),
+    }
+    for name, (res, args) in sigs.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+EXPORTED_SYMBOLS = ("sq_strerror", "sq_last_cuda_error", "sq_version", "sq_validate_key", "sq_keygen",
+                    "sq_fill_u32", "sq_fill_u64", "sq_fill_f32", "sq_fused_stats", "sq_fill_host")
+
+
+def _check(fn: str, code: int) -> None:
+    if code != SQ_OK:
+        raise SquaresError(fn, code)
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _u64(x: int) -> int:
+    return int(x) & M64
+
+
+# ----------------------------------------------------------------------------- host functions
+def version() -> int:
+    return _load().sq_version()
+
+
+def validate_key(key: int) -> int:
+    """Bitmask of violated key rules (0 = valid); see include/squares.h."""
+    return _load().sq_validate_key(_u64(key))
+
+
+def keygen(seed: int, count: int) -> torch.Tensor:
+    """`count` keys of stream `seed` (documented "different digits" mapping), int64 CPU tensor."""
+    out = torch.empty(max(int(count), 1), dtype=torch.int64)
+    _check("sq_keygen", _load().sq_keygen(_u64(seed), int(count), out.data_ptr()))
+    return out[: int(count)]
+
+
+# ----------------------------------------------------------------------------- device functions
+_OUT_DTYPE = {"u32": torch.int32, "u64": torch.int64, "f32": torch.float32}
+
+
+def _fill(kind: str, keys: torch.Tensor, ctr0: int, n: int, out: torch.Tensor | None, ld: int | None,
+          stream=None) -> torch.Tensor:
+    if not (keys.is_cuda and keys.dtype == torch.int64 and keys.dim() == 1 and keys.is_contiguous()):
+        raise ValueError("keys must be a contiguous 1-D int64 CUDA tensor")
+    nkeys = keys.numel()
+    if out is None:
+        ld = n if ld is None else ld
+        out = torch.empty((nkeys, ld), dtype=_OUT_DTYPE[kind], device=keys.device)
+    else:
+        if out.dtype != _OUT_DTYPE[kind] or not out.is_cuda:
+            raise ValueError(f"out must be a CUDA {_OUT_DTYPE[kind]} tensor")
+        if ld is None:
+            ld = out.shape[-1] if out.dim() == 2 else n
+        need = (nkeys - 1) * ld + n if nkeys else 0
+        if out.numel() - 0 < need or not out.is_contiguous():
+            raise ValueError("out is too small or not contiguous")
+    fn = getattr(_load(), f"sq_fill_{kind}")
+    _check(f"sq_fill_{kind}", fn(keys.data_ptr(), nkeys, _u64(ctr0), int(n), out.data_ptr(), int(ld),
+                                 _stream_handle(stream)))
+    return out
+
+
+def fill_u32(keys, ctr0, n, out=None, ld=None, stream=None):
+    """out[k, i] = squares32(ctr0 + i, keys[k]) as int32 bit patterns."""
+    return _fill("u32", keys, ctr0, n, out, ld, stream)
+
+
+def fill_u64(keys, ctr0, n, out=None, ld=None, stream=None):
+    """out[k, i] = squares64(ctr0 + i, keys[k]) as int64 bit patterns."""
+    return _fill("u64", keys, ctr0, n, out, ld, stream)
+
+
+def fill_f32(keys, ctr0, n, out=None, ld=None, stream=None):
+    """out[k, i] = (squares32(ctr0 + i, keys[k]) >> 8) * 2^-24, float32 in [0, 1)."""
+    return _fill("f32", keys, ctr0, n, out, ld, stream)
+
+
+def fused_stats(key: int, ctr0: int, n: int, hist: torch.Tensor | None = None,
+                ones: torch.Tensor | None = None, device=None, stream=None):
+    """Accumulate the top-16-bit histogram (65536 bins) and the 32 per-bit ones counts of
+    squares32 over [ctr0, ctr0 + n) into int64 CUDA tensors (allocated zeroed if None)."""
+    dev = device if device is not None else (hist.device if hist is not None else torch.device("cuda"))
+    if hist is None:
+        hist = torch.zeros(HIST_BINS, dtype=torch.int64, device=dev)
+    if ones is None:
+        ones = torch.zeros(32, dtype=torch.int64, device=dev)
+    for t, sz in ((hist, HIST_BINS), (ones, 32)):
+        if not (t.is_cuda and t.dtype == torch.int64 and t.numel() == sz and t.is_contiguous()):
+            raise ValueError(f"expected a contiguous int64 CUDA tensor of {sz} elements")
+    _check("sq_fused_stats", _load().sq_fused_stats(_u64(key), _u64(ctr0), int(n), hist.data_ptr(),
+                                                    ones.data_ptr(), _stream_handle(stream)))
+    return hist, ones
+
+
+def fill_host(kind: str, key: int, ctr0: int, n: int, out_host: torch.Tensor, scratch: torch.Tensor,
+              stream=None, copy_stream=None) -> torch.Tensor:
+    """End-to-end fill of ONE key into a (pinned) host tensor via the library's chunked
+    generate + D2H pipeline.  Synchronous."""
+    es = 8 if kind == "u64" else 4
+    if out_host.is_cuda or out_host.numel() * out_host.element_size() < n * es:
+        raise ValueError("out_host must be a host tensor of at least n elements")
+    if not scratch.is_cuda:
+        raise ValueError("scratch must be a CUDA tensor")
+    cs = _stream_handle(copy_stream) if copy_stream is not None else None
+    _check("sq_fill_host", _load().sq_fill_host(KINDS[kind], _u64(key), _u64(ctr0), int(n),
+                                                out_host.data_ptr(), scratch.data_ptr(),
+                                                scratch.numel() * scratch.element_size(),
+                                                _stream_handle(stream), cs))
+    return out_host
+
+
+def as_unsigned(t: torch.Tensor):
+    """numpy view of an int32/int64 CPU tensor as uint32/uint64."""
+    import numpy as np
+    a = t.numpy()
+    return a.view(np.uint32) if a.dtype == np.int32 else a.view(np.uint64) if a.dtype == np.int64 else a

@@ -1,0 +1,168 @@
+// capi.cu -- the extern "C" entry points of libsquares.so declared in include/squares.h:
+// argument validation, error codes, device-property cache, and the host-buffer fill.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+
+#include "sq_internal.h"
+
+namespace sq {
+
+static thread_local int g_last_cuda_error = 0;
+
+int set_cuda_error(cudaError_t e) {
+  if (e == cudaSuccess) return SQ_OK;
+  g_last_cuda_error = (int)e;
+  return SQ_ECUDA;
+}
+
+static std::mutex g_dev_mu;
+static DeviceInfo g_dev[64];
+static bool g_dev_ok[64];
+
+const DeviceInfo* device_info() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) { set_cuda_error(e); return nullptr; }
+  if (dev < 0 || dev >= 64) { set_cuda_error(cudaErrorInvalidDevice); return nullptr; }
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (!g_dev_ok[dev]) {
+    DeviceInfo d;
+    d.device = dev;
+    e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) { set_cuda_error(e); return nullptr; }
+    g_dev[dev] = d;
+    g_dev_ok[dev] = true;
+  }
+  return &g_dev[dev];
+}
+
+// nkeys * ld * es must fit size_t and the address range of `out`.
+static bool size_ok(uint64_t nkeys, uint64_t ld, uint64_t es) {
+  if (ld == 0) return true;
+  const unsigned __int128 bytes = (unsigned __int128)nkeys * ld * es;
+  return bytes <= (unsigned __int128)SIZE_MAX;
+}
+
+static int fill_entry(int kind, const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n,
+                      void* out_dev, uint64_t ld, cudaStream_t stream) {
+  const uint64_t es = (kind == KIND_U64) ? 8 : 4;
+  if (n == 0 || nkeys == 0) return SQ_OK;
+  if (!keys_dev || !out_dev) return SQ_EINVAL;
+  if (((uintptr_t)out_dev % es) != 0) return SQ_EINVAL;
+  if (nkeys == 1) ld = n;
+  if (ld < n) return SQ_EINVAL;
+  if (!size_ok(nkeys, ld, es)) return SQ_EINVAL;
+  FillArgs a{};
+  a.keys = keys_dev;
+  a.key_imm = 0;
+  a.ctr0 = ctr0;
+  a.n = n;
+  a.out = (char*)out_dev;
+  a.ld_bytes = ld * es;
+  return launch_fill_kind(kind, a, nkeys, n, stream);
+}
+
+}  // namespace sq
+
+using namespace sq;
+
+extern "C" {
+
+const char* sq_strerror(int code) {
+  switch (code) {
+    case SQ_OK: return "SQ_OK: success";
+    case SQ_EINVAL: return "SQ_EINVAL: invalid argument";
+    case SQ_ERANGE: return "SQ_ERANGE: argument out of range";
+    case SQ_ECUDA: return "SQ_ECUDA: CUDA error";
+    case SQ_ENOMEM: return "SQ_ENOMEM: out of host memory";
+    default: return "unknown squares status code";
+  }
+}
+
+int sq_last_cuda_error(void) { return g_last_cuda_error; }
+
+int sq_version(void) { return 100; }
+
+int sq_fill_u32(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n, uint32_t* out_dev,
+                uint64_t ld, sq_stream_t stream) {
+  return fill_entry(KIND_U32, keys_dev, nkeys, ctr0, n, out_dev, ld, (cudaStream_t)stream);
+}
+
+int sq_fill_u64(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n, uint64_t* out_dev,
+                uint64_t ld, sq_stream_t stream) {
+  return fill_entry(KIND_U64, keys_dev, nkeys, ctr0, n, out_dev, ld, (cudaStream_t)stream);
+}
+
+int sq_fill_f32(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n, float* out_dev,
+                uint64_t ld, sq_stream_t stream) {
+  return fill_entry(KIND_F32, keys_dev, nkeys, ctr0, n, out_dev, ld, (cudaStream_t)stream);
+}
+
+int sq_fused_stats(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist_dev, uint64_t* ones_dev,
+                   sq_stream_t stream) {
+  if (n == 0) return SQ_OK;
+  if (!hist_dev || !ones_dev) return SQ_EINVAL;
+  if (((uintptr_t)hist_dev & 7) || ((uintptr_t)ones_dev & 7)) return SQ_EINVAL;
+  return launch_fused(key, ctr0, n, hist_dev, ones_dev, (cudaStream_t)stream);
+}
+
+int sq_fill_host(int kind, uint64_t key, uint64_t ctr0, uint64_t n, void* out_host, void* scratch_dev,
+                 size_t scratch_bytes, sq_stream_t stream, sq_stream_t copy_stream) {
+  if (kind != KIND_U32 && kind != KIND_U64 && kind != KIND_F32) return SQ_EINVAL;
+  if (n == 0) return SQ_OK;
+  if (!out_host || !scratch_dev) return SQ_EINVAL;
+  const uint64_t es = (kind == KIND_U64) ? 8 : 4;
+  // two ping-pong halves, each a multiple of 32 bytes
+  const uint64_t half = (scratch_bytes / 2) & ~(uint64_t)31;
+  const uint64_t chunk = half / es;
+  if (chunk == 0) return SQ_EINVAL;
+  cudaStream_t gs = (cudaStream_t)stream, cs = (cudaStream_t)copy_stream;
+  if (cs == gs) cs = nullptr;
+  cudaEvent_t gen_done[2], copy_done[2];
+  for (int b = 0; b < 2; b++) {
+    cudaError_t e = cudaEventCreateWithFlags(&gen_done[b], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copy_done[b], cudaEventDisableTiming);
+    if (e != cudaSuccess) return set_cuda_error(e);
+  }
+  int rc = SQ_OK;
+  uint64_t done = 0;
+  int b = 0;
+  bool used[2] = {false, false};
+  while (done < n && rc == SQ_OK) {
+    const uint64_t m = (n - done < chunk) ? (n - done) : chunk;
+    char* buf = (char*)scratch_dev + b * half;
+    cudaError_t e = cudaSuccess;
+    if (used[b]) e = cudaStreamWaitEvent(gs, copy_done[b], 0);   // buffer free again
+    if (e != cudaSuccess) { rc = set_cuda_error(e); break; }
+    FillArgs a{};
+    a.keys = nullptr;
+    a.key_imm = key;
+    a.ctr0 = ctr0 + done;
+    a.n = m;
+    a.out = buf;
+    a.ld_bytes = m * es;
+    rc = launch_fill_kind(kind, a, 1, m, gs);
+    if (rc != SQ_OK) break;
+    cudaStream_t copier = cs ? cs : gs;
+    e = cudaEventRecord(gen_done[b], gs);
+    if (e == cudaSuccess && cs) e = cudaStreamWaitEvent(cs, gen_done[b], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync((char*)out_host + done * es, buf, m * es, cudaMemcpyDeviceToHost, copier);
+    if (e == cudaSuccess) e = cudaEventRecord(copy_done[b], copier);
+    if (e != cudaSuccess) { rc = set_cuda_error(e); break; }
+    used[b] = true;
+    done += m;
+    b ^= 1;
+  }
+  cudaError_t e1 = cudaStreamSynchronize(gs);
+  cudaError_t e2 = cs ? cudaStreamSynchronize(cs) : cudaSuccess;
+  for (int i = 0; i < 2; i++) { cudaEventDestroy(gen_done[i]); cudaEventDestroy(copy_done[i]); }
+  if (rc != SQ_OK) return rc;
+  if (e1 != cudaSuccess) return set_cuda_error(e1);
+  return set_cuda_error(e2);
+}
+
+}  // extern "C"

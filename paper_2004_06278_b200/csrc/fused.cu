@@ -1,0 +1,249 @@
+// fused.cu -- sq_fused_stats: generate squares32 and reduce without storing
+// (BASELINE.json config 5; the GPU analogue of PAPER.md P:45's "basic uniformity test").
+//
+//   hist[b] += #{i : u_i >> 16 == b},  ones[j] += #{i : bit j of u_i},  u_i = squares32(ctr0+i, key)
+//
+// Design:
+//  * One CTA of 1024 threads per SM (persistent), each thread owning one contiguous counter
+//    range, walked with the multiply-free Weyl/finite-difference step (squares_device.cuh).
+//  * hist: a 65536-bin histogram held in shared memory as 16-bit counters packed two per
+//    32-bit word (128 KiB; 32-bit bins would need 256 KiB > 227 KiB).  Exactness by a
+//    guard-bit + epoch scheme: a CTA barrier follows every 32 samples per thread, so at most
+//    1024*32 = 0x8000 increments reach any half per epoch; every half is <= 0x7FFF at an
+//    epoch start, so it never exceeds 0xFFFF (no carry into its neighbour).  The one thread
+//    whose ATOMS.ADD moves a half from 0x7FFF to 0x8000 (seen in the returned old value)
+//    subtracts 0x8000 from that half and adds 0x8000 to the global bin before the next
+//    barrier, restoring the invariant.  Final bin = sum of fix-ups + residual.
+//  * ones[16..31] are derived exactly from the histogram (bit j of u is bit j-16 of its bin):
+//    from the CTA's residual bins and its fix-ups, at the end.
+//  * ones[0..15]: bit-sliced carry-save counting.  Two samples' low halves are packed in one
+//    32-bit word (columns j and j+16 both count bit j); a Harley-Seal tree folds 16 words
+//    (one epoch) into a weight-16 word, which is ripple-added into 6 vertical counter planes,
+//    flushed to shared-memory totals every 63 epochs.  ~1.3 LOP3 per sample.
+//  * At exit: residual bins -> global hist (RED.ADD.64), CTA bit totals -> global ones.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "squares_device.cuh"
+#include "sq_internal.h"
+
+namespace sq {
+
+constexpr int kEpoch = 32;        // samples per thread per epoch (x1024 threads = 0x8000)
+constexpr int kPlanes = 6;        // vertical planes for weight-16 words: counts up to 63
+constexpr int kFlushEvery = 63;   // epochs between plane flushes
+constexpr size_t kFusedSmem = 32768 * 4 + 16 * 8 + 16 * 8 + 16 * 4;
+
+static_assert(kFusedThreads * kEpoch <= 0x8000, "epoch bound of the guard-bit scheme");
+
+struct FusedShared {
+  uint32_t* bins;                 // 32768 words
+  unsigned long long* lo_cnt;     // 16: CTA totals for bits 0..15
+  unsigned long long* hi_cnt;     // 16: CTA totals for bits 16..31 from residual bins
+  uint32_t* fix;                  // 16: fix-ups of bins with bit j set
+};
+
+__device__ __noinline__ void guard_fixup(uint32_t* bins, uint32_t b, uint32_t inc,
+                                         unsigned long long* hist, uint32_t* fix) {
+  atomicSub(&bins[b >> 1], inc << 15);                 // half -= 0x8000
+  atomicAdd(&hist[b], 0x8000ull);
+#pragma unroll 1
+  for (int j = 0; j < 16; j++)
+    if ((b >> j) & 1u) atomicAdd(&fix[j], 1u);
+}
+
+__device__ __forceinline__ void hist_add(uint32_t* bins, uint32_t u, unsigned long long* hist,
+                                         uint32_t* fix) {
+  const uint32_t b = u >> 16;
+  const uint32_t inc = (u & 0x10000u) ? 0x10000u : 1u;
+  const uint32_t old = atomicAdd(&bins[b >> 1], inc);
+  if (((old + inc) ^ old) & 0x80008000u) guard_fixup(bins, b, inc, hist, fix);
+}
+
+// carry-save adder: (h, l) = (maj(a,b,c), a^b^c)
+__device__ __forceinline__ void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32_t b, uint32_t c) {
+  const uint32_t u = a ^ b;
+  h = (a & b) | (u & c);
+  l = u ^ c;
+}
+
+// Adds weight*(count of set bits in columns j and j+16 of `word`) for j = 0..15 into cnt[].
+__device__ __forceinline__ void columns_add(uint32_t (&cnt)[16], uint32_t word, uint32_t weight) {
+#pragma unroll
+  for (int j = 0; j < 16; j++) cnt[j] += (((word >> j) & 1u) + ((word >> (j + 16)) & 1u)) * weight;
+}
+
+__device__ __forceinline__ void warp_flush16(uint32_t (&cnt)[16], unsigned long long* dst) {
+#pragma unroll
+  for (int j = 0; j < 16; j++) {
+    const uint32_t s = __reduce_add_sync(0xffffffffu, cnt[j]);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(&dst[j], (unsigned long long)s);
+    cnt[j] = 0;
+  }
+}
+
+// Two samples (consecutive counters) -> their packed low halves; hist updated.
+template <bool MASKED>
+__device__ __forceinline__ uint32_t two_samples(State& s, uint64_t key, uint64_t k2x2, uint32_t* bins,
+                                                unsigned long long* hist, uint32_t* fix,
+                                                int64_t& rem) {
+  uint32_t ua = squares32_from(s.y, s.y + key, s.u);
+  step(s, key, k2x2);
+  uint32_t ub = squares32_from(s.y, s.y + key, s.u);
+  step(s, key, k2x2);
+  if (MASKED) {
+    if (rem <= 0) ua = 0;
+    else hist_add(bins, ua, hist, fix);
+    if (rem <= 1) ub = 0;
+    else hist_add(bins, ub, hist, fix);
+    rem -= 2;
+  } else {
+    hist_add(bins, ua, hist, fix);
+    hist_add(bins, ub, hist, fix);
+  }
+  return __byte_perm(ua, ub, 0x5410);   // low half of ua | low half of ub << 16
+}
+
+// One epoch (32 samples = 16 packed words) folded by Harley-Seal into a weight-16 word.
+template <bool MASKED>
+__device__ __forceinline__ uint32_t epoch(State& s, uint64_t key, uint64_t k2x2, uint32_t* bins,
+                                          unsigned long long* hist, uint32_t* fix, int64_t rem,
+                                          uint32_t& ones, uint32_t& twos, uint32_t& fours,
+                                          uint32_t& eights) {
+  uint32_t eightsAB[2];
+#pragma unroll
+  for (int blk = 0; blk < 2; blk++) {
+    uint32_t foursAB[2];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      uint32_t twosA, twosB;
+      uint32_t w0 = two_samples<MASKED>(s, key, k2x2, bins, hist, fix, rem);
+      uint32_t w1 = two_samples<MASKED>(s, key, k2x2, bins, hist, fix, rem);
+      csa(twosA, ones, ones, w0, w1);
+      uint32_t w2 = two_samples<MASKED>(s, key, k2x2, bins, hist, fix, rem);
+      uint32_t w3 = two_samples<MASKED>(s, key, k2x2, bins, hist, fix, rem);
+      csa(twosB, ones, ones, w2, w3);
+      csa(foursAB[h], twos, twos, twosA, twosB);
+    }
+    csa(eightsAB[blk], fours, fours, foursAB[0], foursAB[1]);
+  }
+  uint32_t sixteens;
+  csa(sixteens, eights, eights, eightsAB[0], eightsAB[1]);
+  return sixteens;
+}
+
+__global__ void __launch_bounds__(kFusedThreads, 1)
+fused_kernel(uint64_t key, uint64_t ctr0, uint64_t q, uint64_t r, uint32_t epochs,
+             unsigned long long* __restrict__ hist, unsigned long long* __restrict__ ones_out) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  uint32_t* bins = smem;
+  unsigned long long* lo_cnt = (unsigned long long*)(smem + 32768);
+  unsigned long long* hi_cnt = lo_cnt + 16;
+  uint32_t* fix = (uint32_t*)(hi_cnt + 16);
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t i = tid; i < 32768; i += kFusedThreads) bins[i] = 0;
+  if (tid < 16) { lo_cnt[tid] = 0; hi_cnt[tid] = 0; fix[tid] = 0; }
+  __syncthreads();
+
+  const uint64_t t = (uint64_t)blockIdx.x * kFusedThreads + tid;
+  const uint64_t start = t * q + (t < r ? t : r);
+  const uint64_t cnt = q + (t < r ? 1 : 0);
+  State s = state_at(ctr0 + start, key);
+  const uint64_t k2x2 = 2 * key * key;
+
+  uint32_t ones = 0, twos = 0, fours = 0, eights = 0;
+  uint32_t pl[kPlanes];
+#pragma unroll
+  for (int p = 0; p < kPlanes; p++) pl[p] = 0;
+  uint32_t colcnt[16];
+#pragma unroll
+  for (int j = 0; j < 16; j++) colcnt[j] = 0;
+
+  uint64_t done = 0;
+  int since_flush = 0;
+  for (uint32_t ep = 0; ep < epochs; ep++) {
+    uint32_t sixteens;
+    if (done + kEpoch <= cnt) {
+      sixteens = epoch<false>(s, key, k2x2, bins, hist, fix, 0, ones, twos, fours, eights);
+    } else {
+      const int64_t rem = done < cnt ? (int64_t)(cnt - done) : 0;
+      sixteens = epoch<true>(s, key, k2x2, bins, hist, fix, rem, ones, twos, fours, eights);
+    }
+    done += kEpoch;
+    // ripple-add the weight-16 word into the vertical planes
+    uint32_t c = sixteens;
+#pragma unroll
+    for (int p = 0; p < kPlanes; p++) {
+      const uint32_t tt = pl[p] & c;
+      pl[p] ^= c;
+      c = tt;
+    }
+    if (++since_flush == kFlushEvery) {   // planes hold <= 63 per column: flush to the CTA totals
+      since_flush = 0;
+#pragma unroll
+      for (int p = 0; p < kPlanes; p++) { columns_add(colcnt, pl[p], 16u << p); pl[p] = 0; }
+      warp_flush16(colcnt, lo_cnt);
+    }
+    __syncthreads();   // epoch boundary of the guard-bit scheme
+  }
+  // remaining carry-save state: weights 1, 2, 4, 8 and the planes
+  columns_add(colcnt, ones, 1);
+  columns_add(colcnt, twos, 2);
+  columns_add(colcnt, fours, 4);
+  columns_add(colcnt, eights, 8);
+#pragma unroll
+  for (int p = 0; p < kPlanes; p++) columns_add(colcnt, pl[p], 16u << p);
+  warp_flush16(colcnt, lo_cnt);
+
+  // residual bins -> global hist; bits 16..31 derived from the residual bins.
+  // Thread tid owns words [32*tid, 32*tid+32) = bins [64*tid, 64*tid+64): bins' bits 6..15
+  // are tid's bits; the word index i (rotated by lane for conflict-free banks) gives bits 1..5.
+  uint32_t T = 0, S[6] = {0, 0, 0, 0, 0, 0};
+  const uint32_t lane = tid & 31;
+#pragma unroll 4
+  for (uint32_t k = 0; k < 32; k++) {
+    const uint32_t i = (k + lane) & 31;
+    const uint32_t wv = bins[32 * tid + i];
+    const uint32_t lo = wv & 0xFFFFu, hi = wv >> 16;
+    const uint32_t b0 = 64 * tid + 2 * i;
+    if (lo) atomicAdd(&hist[b0], (unsigned long long)lo);
+    if (hi) atomicAdd(&hist[b0 + 1], (unsigned long long)hi);
+    T += lo + hi;
+    S[0] += hi;
+#pragma unroll
+    for (int j = 1; j < 6; j++) S[j] += ((i >> (j - 1)) & 1u) ? (lo + hi) : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < 16; j++) colcnt[j] = (j < 6) ? S[j] : (((tid >> (j - 6)) & 1u) ? T : 0u);
+  warp_flush16(colcnt, hi_cnt);
+  __syncthreads();
+  if (tid < 16) {
+    const unsigned long long lo = lo_cnt[tid];
+    const unsigned long long hi = hi_cnt[tid] + 0x8000ull * (unsigned long long)fix[tid];
+    if (lo) atomicAdd(&ones_out[tid], lo);
+    if (hi) atomicAdd(&ones_out[16 + tid], hi);
+  }
+}
+
+int launch_fused(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist, uint64_t* ones,
+                 cudaStream_t stream) {
+  const DeviceInfo* di = device_info();
+  if (!di) return SQ_ECUDA;
+  cudaError_t e = cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kFusedSmem);
+  if (e != cudaSuccess) return set_cuda_error(e);
+  // one CTA per SM; small n uses fewer CTAs (>= 2^20 samples each) so the flush amortises
+  uint64_t blocks = (n + (1ull << 20) - 1) >> 20;
+  if (blocks > (uint64_t)di->sms) blocks = di->sms;
+  if (blocks < 1) blocks = 1;
+  const uint64_t T = blocks * kFusedThreads;
+  const uint64_t q = n / T, r = n % T;
+  const uint64_t per = q + (r ? 1 : 0);
+  const uint64_t epochs = (per + kEpoch - 1) / kEpoch;
+  if (epochs > 0xFFFFFFFFull) return SQ_ERANGE;
+  fused_kernel<<<(unsigned)blocks, kFusedThreads, kFusedSmem, stream>>>(
+      key, ctr0, q, r, (uint32_t)epochs, (unsigned long long*)hist, (unsigned long long*)ones);
+  return set_cuda_error(cudaGetLastError());
+}
+
+}  // namespace sq

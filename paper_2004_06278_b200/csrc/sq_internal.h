@@ -1,0 +1,43 @@
+// sq_internal.h -- shared declarations of libsquares.so (not part of the public ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/squares.h"
+
+namespace sq {
+
+enum Kind { KIND_U32 = 0, KIND_U64 = 1, KIND_F32 = 2 };
+
+constexpr int kFillThreads = 256;
+constexpr int kFusedThreads = 1024;
+
+struct FillArgs {
+  const uint64_t* keys;     // device keys, or nullptr to use key_imm (single row)
+  uint64_t key_imm;
+  uint64_t ctr0;
+  uint64_t n;
+  char* out;                // row 0 base
+  uint64_t ld_bytes;        // row pitch in bytes
+  uint64_t chunks_per_row;  // set by the launcher
+  uint64_t chunks_q, chunks_r;  // balanced split of all chunks over the grid's warps
+};
+
+struct DeviceInfo {
+  int device;
+  int sms;
+  int smem_optin;
+};
+
+// Cached per-device properties of the current device (nullptr + error recorded on failure).
+const DeviceInfo* device_info();
+
+// Record a CUDA error for sq_last_cuda_error(); returns SQ_OK for cudaSuccess else SQ_ECUDA.
+int set_cuda_error(cudaError_t e);
+
+int launch_fill_kind(int kind, const FillArgs& a, uint64_t nkeys, uint64_t n, cudaStream_t stream);
+
+int launch_fused(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist, uint64_t* ones,
+                 cudaStream_t stream);
+
+}  // namespace sq

@@ -1,0 +1,242 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI vs the CPU oracle, element by element.
+
+Bar (BASELINE.json north_star): bit-exact for every u32/u64 output, every float32 (a
+deterministic integer->float map) and every count.  Inputs are seeded and synthetic
+(synth_inputs.py); keys come from the ORACLE's key utility so no oracle input is produced by the
+product.  Sizes: small cases span several warp chunks and ragged tails; the full-size configs of
+BASELINE.json (c2, c3, c4) are compared in full against the oracle run on all host cores; c5
+(2^38 counters) is checked by invariants plus oracle parity on sampled sub-ranges.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth_inputs as SI
+from tests.helpers import first_mismatch, par_fill, par_fused
+
+pytestmark = pytest.mark.gpu
+
+M64 = (1 << 64) - 1
+VIEW = {"u32": np.uint32, "u64": np.uint64, "f32": np.uint32}
+
+
+@pytest.fixture(scope="module")
+def sq():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2004_06278_b200 as sq
+    torch.cuda.set_device(0)
+    return sq
+
+
+def _dev_keys(keys_np):
+    return torch.from_numpy(np.ascontiguousarray(keys_np, dtype=np.uint64).view(np.int64)).cuda()
+
+
+def _bits(t: torch.Tensor, kind):
+    return t.cpu().numpy().view(VIEW[kind])
+
+
+# ----------------------------------------------------------------------------- fills, small
+@pytest.mark.parametrize("kind", ["u32", "u64", "f32"])
+def test_fill_c1_full(sq, kind):
+    """BASELINE.json config 1 shape (2^20 counters, key from seed 1) for every kind."""
+    key = int(O.keygen(1, 1)[0])
+    out = getattr(sq, f"fill_{kind}")(_dev_keys([key]), 0, 1 << 20)
+    torch.cuda.synchronize()
+    got = _bits(out, kind)[0]
+    want = O.fill(kind, [key], 0, 1 << 20)[0].view(VIEW[kind])
+    assert np.array_equal(got, want), first_mismatch(got, want)
+
+
+@pytest.mark.parametrize("kind", ["u32", "u64", "f32"])
+@pytest.mark.parametrize("edge", SI.FILL_EDGES)
+def test_fill_edges(sq, kind, edge):
+    """n = 0/1/3/5, counter wrap at 2^64, 32-bit counter carry, ragged tails, misaligned output
+    pointer, multi-key rows with padding (sentinel check: padding must stay untouched)."""
+    ctr0, n, nkeys, ld_pad, off = edge
+    keys = O.keygen(11, nkeys)
+    ld = n + ld_pad
+    es = 8 if kind == "u64" else 4
+    dt = {"u32": torch.int32, "u64": torch.int64, "f32": torch.float32}[kind]
+    total = off + nkeys * ld + 64
+    sentinel = torch.full((total,), -1, dtype=torch.int32 if es == 4 else torch.int64).view(dt).cuda()
+    view = sentinel[off: off + nkeys * ld]
+    getattr(sq, f"fill_{kind}")(_dev_keys(keys), ctr0, n, out=view, ld=ld)
+    torch.cuda.synchronize()
+    allbits = sentinel.cpu().numpy().view(VIEW[kind])
+    fill_val = VIEW[kind](-1 & (M64 if es == 8 else 0xFFFFFFFF))
+    want = O.fill(kind, keys, ctr0, n, ld=ld).view(VIEW[kind])
+    got = allbits[off: off + nkeys * ld].reshape(nkeys, ld) if nkeys * ld else np.zeros((nkeys, 0), VIEW[kind])
+    for k in range(nkeys):
+        assert np.array_equal(got[k, :n], want[k, :n]), (k, first_mismatch(got[k, :n], want[k, :n]))
+        assert (got[k, n:] == fill_val).all(), "padding between rows was written"
+    assert (allbits[:off] == fill_val).all() and (allbits[off + nkeys * ld:] == fill_val).all()
+
+
+@pytest.mark.parametrize("kind", ["u32", "u64"])
+def test_fill_corner_keys(sq, kind):
+    """Kernels are total over (ctr, key): key 0, 1, 2^32, 2^64-1 and random odd/even."""
+    keys = np.array([0, 1, 1 << 32, M64, 0x123456789ABCDEF3] + SI.random_u64(3, 5).tolist(), dtype=np.uint64)
+    for ctr0 in (0, (1 << 32) - 100, M64 - 300):
+        out = getattr(sq, f"fill_{kind}")(_dev_keys(keys), ctr0, 777)
+        torch.cuda.synchronize()
+        got = _bits(out, kind)
+        want = O.fill(kind, keys, ctr0, 777).view(VIEW[kind])
+        assert np.array_equal(got, want)
+
+
+def test_fill_random_pairs(sq):
+    """Fuzz: seeded random (ctr, key) pairs plus the full corner cross product, each evaluated
+    as a short fill row starting at that counter (so the state initialisation at an arbitrary
+    counter and the first steps are exercised for every pair)."""
+    ctr, key = SI.random_pairs(2000, seed=SI.FUZZ_SEED)
+    for j in range(ctr.size):
+        c, k = int(ctr[j]), int(key[j])
+        o32 = _bits(sq.fill_u32(_dev_keys([k]), c, 3), "u32")[0]
+        o64 = _bits(sq.fill_u64(_dev_keys([k]), c, 3), "u64")[0]
+        for i in range(3):
+            assert o32[i] == O.squares32((c + i) & M64, k), (hex(c), hex(k), i)
+            assert o64[i] == O.squares64((c + i) & M64, k), (hex(c), hex(k), i)
+
+
+def test_gpu_hi32_of_u64_equals_u32(sq):
+    """P:62-63 vs P:27 on the GPU outputs themselves."""
+    keys = _dev_keys(O.keygen(3, 2))
+    a = sq.fill_u32(keys, 5, 100_003)
+    b = sq.fill_u64(keys, 5, 100_003)
+    torch.cuda.synchronize()
+    assert np.array_equal((_bits(b, "u64") >> np.uint64(32)).astype(np.uint32), _bits(a, "u32"))
+
+
+def test_fill_stream_semantics(sq):
+    """Asynchronous on the caller's stream: a side stream's result is visible after its sync."""
+    s = torch.cuda.Stream()
+    keys = _dev_keys(O.keygen(1, 1))
+    with torch.cuda.stream(s):
+        out = sq.fill_u32(keys, 0, 1 << 16)
+    s.synchronize()
+    want = O.fill("u32", O.keygen(1, 1), 0, 1 << 16)
+    assert np.array_equal(_bits(out, "u32"), want)
+
+
+# ----------------------------------------------------------------------------- fills, full size
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_fill_full_size_single_key(sq, cfg):
+    """BASELINE.json configs 2 and 3 at full size (4 GiB each), compared in full."""
+    w = SI.CONFIGS[cfg]
+    key = int(O.keygen(w.key_seed, 1)[0])
+    out = getattr(sq, f"fill_{w.kind}")(_dev_keys([key]), w.ctr0, w.n)
+    torch.cuda.synchronize()
+    got = _bits(out, w.kind)[0]
+    del out
+    want = par_fill(w.kind, key, w.ctr0, w.n).view(VIEW[w.kind])
+    assert np.array_equal(got, want), first_mismatch(got, want)
+
+
+def test_fill_full_size_c4(sq):
+    """BASELINE.json config 4: 4096 keys (seed 7) x 2^18 counters as float32, [key][ctr]."""
+    w = SI.CONFIGS["c4"]
+    keys = O.keygen(w.key_seed, w.nkeys)
+    out = sq.fill_f32(_dev_keys(keys), w.ctr0, w.n)
+    torch.cuda.synchronize()
+    got = _bits(out, "f32")
+    del out
+    from concurrent.futures import ThreadPoolExecutor
+    from tests.helpers import ncores
+    with ThreadPoolExecutor(ncores()) as ex:
+        rows = list(ex.map(lambda k: O.fill("f32", [int(k)], w.ctr0, w.n)[0], keys))
+    want = np.stack(rows).view(np.uint32)
+    assert np.array_equal(got, want), first_mismatch(got.reshape(-1), want.reshape(-1))
+    f = got.view(np.float32)
+    assert f.min() >= 0.0 and f.max() < 1.0
+
+
+# ----------------------------------------------------------------------------- fused statistics
+def _fused(sq, key, ctr0, n):
+    h, o = sq.fused_stats(key, ctr0, n)
+    torch.cuda.synchronize()
+    return h.cpu().numpy().view(np.uint64), o.cpu().numpy().view(np.uint64)
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 33, 1000, 32768 * 3 + 7, (1 << 20) + 5, 1 << 22])
+def test_fused_small(sq, n):
+    key = int(O.keygen(1, 1)[0])
+    h, o = _fused(sq, key, 77, n)
+    hw, ow = O.fused_stats(key, 77, n)
+    assert np.array_equal(h, hw), first_mismatch(h, hw)
+    assert np.array_equal(o, ow), first_mismatch(o, ow)
+
+
+def test_fused_accumulates(sq):
+    key = int(O.keygen(1, 1)[0])
+    h = torch.zeros(65536, dtype=torch.int64, device="cuda")
+    o = torch.zeros(32, dtype=torch.int64, device="cuda")
+    for start, ln in [(0, 100_000), (100_000, 1 << 20), (100_000 + (1 << 20), 12345)]:
+        sq.fused_stats(key, start, ln, h, o)
+    torch.cuda.synchronize()
+    hw, ow = O.fused_stats(key, 0, 100_000 + (1 << 20) + 12345)
+    assert np.array_equal(h.cpu().numpy().view(np.uint64), hw)
+    assert np.array_equal(o.cpu().numpy().view(np.uint64), ow)
+
+
+def test_fused_key_zero_guard_path(sq):
+    """key = 0: every sample lands in bin 0, driving the guard-bit fix-up path ~2^24/2^15 times
+    per CTA; closed form hist[0] = n, ones = 0."""
+    n = 1 << 26
+    h, o = _fused(sq, 0, 5, n)
+    assert h[0] == n and h[1:].sum() == 0 and o.sum() == 0
+
+
+def test_fused_hot_bins_both_halves(sq):
+    """key = 2^32: outputs concentrate on few bins for small counters (closed form family);
+    checks fix-ups in both 16-bit halves against the oracle."""
+    n = 1 << 23
+    h, o = _fused(sq, 1 << 32, 0, n)
+    hw, ow = O.fused_stats(1 << 32, 0, n)
+    assert np.array_equal(h, hw) and np.array_equal(o, ow)
+
+
+def test_fused_2_30_vs_parallel_oracle(sq):
+    key = int(O.keygen(1, 1)[0])
+    n = 1 << 30
+    h, o = _fused(sq, key, 0, n)
+    hw, ow = par_fused(key, 0, n)
+    assert np.array_equal(h, hw), first_mismatch(h, hw)
+    assert np.array_equal(o, ow), first_mismatch(o, ow)
+
+
+def test_fused_c5_full_size(sq):
+    """BASELINE.json config 5 (2^38 counters, one GPU): invariants at full size, and oracle
+    parity on sampled sub-ranges (the fused map is additive over counter ranges)."""
+    w = SI.CONFIGS["c5"]
+    key = int(O.keygen(w.key_seed, 1)[0])
+    h, o = _fused(sq, key, w.ctr0, w.n)
+    assert int(h.sum()) == w.n
+    b = np.arange(65536, dtype=np.uint64)
+    for j in range(16):
+        assert int(o[16 + j]) == int(h[(b >> np.uint64(j)) & np.uint64(1) == 1].sum())
+    # plausibility bands (not parity): E[hist] = 2^22, sd ~ 2^11; E[ones] = 2^37, sd = 2^18
+    assert abs(h.astype(np.float64).mean() - 2 ** 22) < 1
+    assert np.abs(h.astype(np.float64) - 2 ** 22).max() < 12 * 2 ** 11
+    assert np.abs(o.astype(np.float64) - 2 ** 37).max() < 8 * 2 ** 18
+    # sampled sub-ranges at the start, the middle and the end of the counter range
+    for start in (0, (1 << 37) + 12345, w.n - (1 << 24)):
+        hs, os_ = _fused(sq, key, start, 1 << 24)
+        hw, ow = par_fused(key, start, 1 << 24)
+        assert np.array_equal(hs, hw) and np.array_equal(os_, ow), start
+
+
+def test_fill_host_e2e(sq):
+    """sq_fill_host: chunked generate + D2H into pinned host memory equals the oracle."""
+    key = int(O.keygen(1, 1)[0])
+    n = (1 << 22) + 3
+    scratch = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    for kind in ("u32", "u64", "f32"):
+        es = 8 if kind == "u64" else 4
+        host = torch.empty(n * es, dtype=torch.uint8).pin_memory()
+        sq.fill_host(kind, key, 99, n, host, scratch, copy_stream=torch.cuda.Stream())
+        got = host.numpy().view(VIEW[kind])
+        want = O.fill(kind, [key], 99, n)[0].view(VIEW[kind])
+        assert np.array_equal(got, want), (kind, first_mismatch(got, want))
