@@ -206,10 +206,18 @@ def run_ours(args, w: SI.Workload, rank: int, world: int, dev: int):
     else:
         out = torch.empty((kn, n), dtype={"u32": torch.int32, "u64": torch.int64, "f32": torch.float32}[w.kind],
                           device=dev)
-        fill = getattr(sq, f"fill_{w.kind}")
+        if kn == 1:
+            # single key: the by-value entry point (sq_fill_*_k), key in the launch parameters
+            fill_k = getattr(sq, f"fill_{w.kind}_k")
+            out1 = out.view(-1)
 
-        def step():
-            fill(keys_d, ctr0, n, out=out, stream=stream)
+            def step():
+                fill_k(key0, ctr0, n, out=out1, stream=stream)
+        else:
+            fill = getattr(sq, f"fill_{w.kind}")
+
+            def step():
+                fill(keys_d, ctr0, n, out=out, stream=stream)
 
     for _ in range(args.warmup):
         step()

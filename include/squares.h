@@ -113,6 +113,13 @@ int sq_fill_u64(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_
 int sq_fill_f32(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n,
                 float* out_dev, uint64_t ld, sq_stream_t stream);
 
+/* Single-key fills with the key passed BY VALUE (same map, one row, ld = n).  The key travels
+ * in the launch parameters, so the kernel holds it and every per-key constant of the counter
+ * walk in uniform registers.  Same errors as above (no keys pointer to check). */
+int sq_fill_u32_k(uint64_t key, uint64_t ctr0, uint64_t n, uint32_t* out_dev, sq_stream_t stream);
+int sq_fill_u64_k(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* out_dev, sq_stream_t stream);
+int sq_fill_f32_k(uint64_t key, uint64_t ctr0, uint64_t n, float* out_dev, sq_stream_t stream);
+
 /* ----------------------------------------------------------------------------------------
  * Fused generate-and-reduce (BASELINE.json config 5; the GPU analogue of P:45's "basic
  * uniformity test").  With u_i = squares32(ctr0 + i mod 2^64, key), i < n, ACCUMULATES

@@ -60,6 +60,9 @@ def _load() -> ctypes.CDLL:
         "sq_fill_u32": (i32, [vp, u64, u64, u64, vp, u64, vp]),
         "sq_fill_u64": (i32, [vp, u64, u64, u64, vp, u64, vp]),
         "sq_fill_f32": (i32, [vp, u64, u64, u64, vp, u64, vp]),
+        "sq_fill_u32_k": (i32, [u64, u64, u64, vp, vp]),
+        "sq_fill_u64_k": (i32, [u64, u64, u64, vp, vp]),
+        "sq_fill_f32_k": (i32, [u64, u64, u64, vp, vp]),
         "sq_fused_stats": (i32, [u64, u64, u64, vp, vp, vp]),
         "sq_fill_host": (i32, [i32, u64, u64, u64, vp, vp, ctypes.c_size_t, vp, vp]),
     }
@@ -72,7 +75,8 @@ def _load() -> ctypes.CDLL:
 
 
 EXPORTED_SYMBOLS = ("sq_strerror", "sq_last_cuda_error", "sq_version", "sq_validate_key", "sq_keygen",
-                    "sq_fill_u32", "sq_fill_u64", "sq_fill_f32", "sq_fused_stats", "sq_fill_host")
+                    "sq_fill_u32", "sq_fill_u64", "sq_fill_f32", "sq_fill_u32_k", "sq_fill_u64_k",
+                    "sq_fill_f32_k", "sq_fused_stats", "sq_fill_host")
 
 
 def _check(fn: str, code: int) -> None:
@@ -131,6 +135,32 @@ def _fill(kind: str, keys: torch.Tensor, ctr0: int, n: int, out: torch.Tensor | 
     _check(f"sq_fill_{kind}", fn(keys.data_ptr(), nkeys, _u64(ctr0), int(n), out.data_ptr(), int(ld),
                                  _stream_handle(stream)))
     return out
+
+
+def _fill_k(kind: str, key: int, ctr0: int, n: int, out: torch.Tensor | None, device=None,
+            stream=None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(int(n), dtype=_OUT_DTYPE[kind], device=device if device is not None else "cuda")
+    elif out.dtype != _OUT_DTYPE[kind] or not out.is_cuda or not out.is_contiguous() or out.numel() < n:
+        raise ValueError(f"out must be a contiguous CUDA {_OUT_DTYPE[kind]} tensor of >= n elements")
+    fn = getattr(_load(), f"sq_fill_{kind}_k")
+    _check(f"sq_fill_{kind}_k", fn(_u64(key), _u64(ctr0), int(n), out.data_ptr(), _stream_handle(stream)))
+    return out
+
+
+def fill_u32_k(key, ctr0, n, out=None, device=None, stream=None):
+    """Single-key fill, key by value: out[i] = squares32(ctr0 + i, key)."""
+    return _fill_k("u32", key, ctr0, n, out, device, stream)
+
+
+def fill_u64_k(key, ctr0, n, out=None, device=None, stream=None):
+    """Single-key fill, key by value: out[i] = squares64(ctr0 + i, key)."""
+    return _fill_k("u64", key, ctr0, n, out, device, stream)
+
+
+def fill_f32_k(key, ctr0, n, out=None, device=None, stream=None):
+    """Single-key fill, key by value: out[i] = (squares32(ctr0 + i, key) >> 8) * 2^-24."""
+    return _fill_k("f32", key, ctr0, n, out, device, stream)
 
 
 def fill_u32(keys, ctr0, n, out=None, ld=None, stream=None):

@@ -101,6 +101,34 @@ int sq_fill_f32(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_
   return fill_entry(KIND_F32, keys_dev, nkeys, ctr0, n, out_dev, ld, (cudaStream_t)stream);
 }
 
+static int fill_key_entry(int kind, uint64_t key, uint64_t ctr0, uint64_t n, void* out_dev, cudaStream_t stream) {
+  const uint64_t es = (kind == KIND_U64) ? 8 : 4;
+  if (n == 0) return SQ_OK;
+  if (!out_dev) return SQ_EINVAL;
+  if (((uintptr_t)out_dev % es) != 0) return SQ_EINVAL;
+  if (!size_ok(1, n, es)) return SQ_EINVAL;
+  FillArgs a{};
+  a.keys = nullptr;
+  a.key_imm = key;
+  a.ctr0 = ctr0;
+  a.n = n;
+  a.out = (char*)out_dev;
+  a.ld_bytes = n * es;
+  return launch_fill_kind(kind, a, 1, n, stream);
+}
+
+int sq_fill_u32_k(uint64_t key, uint64_t ctr0, uint64_t n, uint32_t* out_dev, sq_stream_t stream) {
+  return fill_key_entry(KIND_U32, key, ctr0, n, out_dev, (cudaStream_t)stream);
+}
+
+int sq_fill_u64_k(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* out_dev, sq_stream_t stream) {
+  return fill_key_entry(KIND_U64, key, ctr0, n, out_dev, (cudaStream_t)stream);
+}
+
+int sq_fill_f32_k(uint64_t key, uint64_t ctr0, uint64_t n, float* out_dev, sq_stream_t stream) {
+  return fill_key_entry(KIND_F32, key, ctr0, n, out_dev, (cudaStream_t)stream);
+}
+
 int sq_fused_stats(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist_dev, uint64_t* ones_dev,
                    sq_stream_t stream) {
   if (n == 0) return SQ_OK;

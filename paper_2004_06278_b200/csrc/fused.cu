@@ -82,31 +82,51 @@ __device__ __forceinline__ void warp_flush16(uint32_t (&cnt)[16], unsigned long 
   }
 }
 
-// Two samples (consecutive counters) -> their packed low halves; hist updated.
-template <bool MASKED>
-__device__ __forceinline__ uint32_t two_samples(State& s, uint64_t key, uint64_t k2x2, uint32_t* bins,
-                                                unsigned long long* hist, uint32_t* fix,
-                                                int64_t& rem) {
-  uint32_t ua = squares32_from(s.y, s.y + key, s.u);
-  step(s, key, k2x2);
-  uint32_t ub = squares32_from(s.y, s.y + key, s.u);
-  step(s, key, k2x2);
-  if (MASKED) {
-    if (rem <= 0) ua = 0;
-    else hist_add(bins, ua, hist, fix);
-    if (rem <= 1) ub = 0;
-    else hist_add(bins, ub, hist, fix);
-    rem -= 2;
-  } else {
-    hist_add(bins, ua, hist, fix);
-    hist_add(bins, ub, hist, fix);
+// Per-key constants of the counter walk: cst[j] = j*2k^2 (j < 8), cst8 = 8*2k^2.
+struct WalkConst {
+  uint64_t key;
+  uint64_t cst[8];
+  uint64_t cst8;
+};
+
+// 8 consecutive samples from state s; s advances by 8 counters.  u uses the 3-input step
+// u(c+j+1) = u(c+j) + e(c) + j*2k^2 (squares_device.cuh), e advances once per group.
+__device__ __forceinline__ void gen8(State& s, const WalkConst& wc, uint32_t (&v)[8]) {
+  uint64_t y = s.y, u = s.u;
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    const uint64_t z = add64(y, wc.key);
+    v[j] = squares32_from(y, z, u);
+    y = z;
+    u = j ? add64_3(u, s.e, wc.cst[j]) : add64(u, s.e);
   }
-  return __byte_perm(ua, ub, 0x5410);   // low half of ua | low half of ub << 16
+  s.y = y;
+  s.u = u;
+  s.e = add64(s.e, wc.cst8);
+}
+
+// Histogram updates for 8 samples (masked ones skipped) and their packed low halves:
+// w[i] = low half of v[2i] | low half of v[2i+1] << 16 (masked samples contribute 0).
+template <bool MASKED>
+__device__ __forceinline__ void reduce8(const uint32_t (&v)[8], uint32_t (&w)[4], uint32_t* bins,
+                                        unsigned long long* hist, uint32_t* fix, int64_t base_rem) {
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    uint32_t a = v[2 * i], b = v[2 * i + 1];
+    if (MASKED) {
+      if (base_rem > 2 * i) hist_add(bins, a, hist, fix); else a = 0;
+      if (base_rem > 2 * i + 1) hist_add(bins, b, hist, fix); else b = 0;
+    } else {
+      hist_add(bins, a, hist, fix);
+      hist_add(bins, b, hist, fix);
+    }
+    w[i] = __byte_perm(a, b, 0x5410);
+  }
 }
 
 // One epoch (32 samples = 16 packed words) folded by Harley-Seal into a weight-16 word.
 template <bool MASKED>
-__device__ __forceinline__ uint32_t epoch(State& s, uint64_t key, uint64_t k2x2, uint32_t* bins,
+__device__ __forceinline__ uint32_t epoch(State& s, const WalkConst& wc, uint32_t* bins,
                                           unsigned long long* hist, uint32_t* fix, int64_t rem,
                                           uint32_t& ones, uint32_t& twos, uint32_t& fours,
                                           uint32_t& eights) {
@@ -116,13 +136,11 @@ __device__ __forceinline__ uint32_t epoch(State& s, uint64_t key, uint64_t k2x2,
     uint32_t foursAB[2];
 #pragma unroll
     for (int h = 0; h < 2; h++) {
-      uint32_t twosA, twosB;
-      uint32_t w0 = two_samples<MASKED>(s, key, k2x2, bins, hist, fix, rem);
-      uint32_t w1 = two_samples<MASKED>(s, key, k2x2, bins, hist, fix, rem);
-      csa(twosA, ones, ones, w0, w1);
-      uint32_t w2 = two_samples<MASKED>(s, key, k2x2, bins, hist, fix, rem);
-      uint32_t w3 = two_samples<MASKED>(s, key, k2x2, bins, hist, fix, rem);
-      csa(twosB, ones, ones, w2, w3);
+      uint32_t v[8], w[4], twosA, twosB;
+      gen8(s, wc, v);
+      reduce8<MASKED>(v, w, bins, hist, fix, rem - 8 * (2 * blk + h));
+      csa(twosA, ones, ones, w[0], w[1]);
+      csa(twosB, ones, ones, w[2], w[3]);
       csa(foursAB[h], twos, twos, twosA, twosB);
     }
     csa(eightsAB[blk], fours, fours, foursAB[0], foursAB[1]);
@@ -149,7 +167,15 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t q, uint64_t r, uint32_t epoch
   const uint64_t start = t * q + (t < r ? t : r);
   const uint64_t cnt = q + (t < r ? 1 : 0);
   State s = state_at(ctr0 + start, key);
-  const uint64_t k2x2 = 2 * key * key;
+  WalkConst wc;
+  {
+    const uint64_t k2x2 = 2 * key * key;
+    wc.key = key;
+    wc.cst[0] = 0;
+#pragma unroll
+    for (int j = 1; j < 8; j++) wc.cst[j] = wc.cst[j - 1] + k2x2;
+    wc.cst8 = wc.cst[7] + k2x2;
+  }
 
   uint32_t ones = 0, twos = 0, fours = 0, eights = 0;
   uint32_t pl[kPlanes];
@@ -164,10 +190,10 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t q, uint64_t r, uint32_t epoch
   for (uint32_t ep = 0; ep < epochs; ep++) {
     uint32_t sixteens;
     if (done + kEpoch <= cnt) {
-      sixteens = epoch<false>(s, key, k2x2, bins, hist, fix, 0, ones, twos, fours, eights);
+      sixteens = epoch<false>(s, wc, bins, hist, fix, kEpoch, ones, twos, fours, eights);
     } else {
       const int64_t rem = done < cnt ? (int64_t)(cnt - done) : 0;
-      sixteens = epoch<true>(s, key, k2x2, bins, hist, fix, rem, ones, twos, fours, eights);
+      sixteens = epoch<true>(s, wc, bins, hist, fix, rem, ones, twos, fours, eights);
     }
     done += kEpoch;
     // ripple-add the weight-16 word into the vertical planes

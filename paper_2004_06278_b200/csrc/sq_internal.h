@@ -9,7 +9,14 @@ namespace sq {
 
 enum Kind { KIND_U32 = 0, KIND_U64 = 1, KIND_F32 = 2 };
 
-constexpr int kFillThreads = 256;
+#ifndef SQ_FILL_THREADS
+#define SQ_FILL_THREADS 256
+#endif
+#ifndef SQ_FILL_MINBLOCKS
+#define SQ_FILL_MINBLOCKS 1
+#endif
+constexpr int kFillThreads = SQ_FILL_THREADS;
+constexpr int kFillMinBlocks = SQ_FILL_MINBLOCKS;
 constexpr int kFusedThreads = 1024;
 
 struct FillArgs {

@@ -41,6 +41,22 @@ __device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
 __device__ __forceinline__ uint32_t lo32(uint64_t v) { return (uint32_t)v; }
 __device__ __forceinline__ uint32_t hi32(uint64_t v) { return (uint32_t)(v >> 32); }
 
+// 64-bit add through inline PTX: opaque to NVVM's induction-variable analysis, which would
+// otherwise rewrite the stepped sequences into closed forms (u_j = u_0 + j*e_0 + ...) that
+// cost extra IMADs on the FMA-heavy pipe -- the pipe that bounds this kernel.
+__device__ __forceinline__ uint64_t add64(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.u64 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// a + b + c mod 2^64 (one IADD3 with two carry-outs + one IADD3.X).
+__device__ __forceinline__ uint64_t add64_3(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("add.u64 %0, %1, %2;\n\tadd.u64 %0, %0, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
 // x <- rot32(x*x + w), x held as (xh, xl).  P:24-26.
 __device__ __forceinline__ void round_rot(uint32_t& xh, uint32_t& xl, uint64_t w) {
   uint64_t t = mad_wide(xl, xl, w);
@@ -58,21 +74,21 @@ __device__ __forceinline__ uint32_t round_hi(uint32_t xh, uint32_t xl, uint64_t 
 // squares32 given y = ctr*key, z = y + key and u = y*y + y (round 1's sum).  P:21-28.
 __device__ __forceinline__ uint32_t squares32_from(uint64_t y, uint64_t z, uint64_t u) {
   uint32_t xh = lo32(u), xl = hi32(u);  // round 1: rot32(u)
-  round_rot(xh, xl, z);                 // round 2
-  round_rot(xh, xl, y);                 // round 3
-  return round_hi(xh, xl, z);           // round 4
+  round_rot(xh, xl, z);             // round 2
+  round_rot(xh, xl, y);             // round 3
+  return round_hi(xh, xl, z);       // round 4
 }
 
 // squares64 given y, z, u as above.  P:56-64: t = x*x + z (round 4, kept before rotating),
 // result t ^ ((rot32(t)^2 + y) >> 32); only t's low half changes.
 __device__ __forceinline__ uint64_t squares64_from(uint64_t y, uint64_t z, uint64_t u) {
   uint32_t xh = lo32(u), xl = hi32(u);
-  round_rot(xh, xl, z);                 // round 2
-  round_rot(xh, xl, y);                 // round 3
+  round_rot(xh, xl, z);             // round 2
+  round_rot(xh, xl, y);             // round 3
   uint64_t t = mad_wide(xl, xl, z);     // round 4 (full 64-bit sum)
   uint32_t th = mad_lo(xl, xh << 1, hi32(t));
   uint32_t tl = lo32(t);
-  uint32_t r5 = round_hi(tl, th, y);    // round 5 on rot32(t) = (tl, th)
+  uint32_t r5 = round_hi(tl, th, y);  // round 5 on rot32(t) = (tl, th)
   return ((uint64_t)th << 32) | (uint64_t)(tl ^ r5);
 }
 
@@ -91,15 +107,6 @@ __device__ __forceinline__ State state_at(uint64_t c, uint64_t k) {
   return s;
 }
 
-// 64-bit add through inline PTX: opaque to NVVM's induction-variable analysis, which would
-// otherwise rewrite the stepped sequences into closed forms (u_j = u_0 + j*e_0 + ...) that
-// cost extra IMADs on the FMA pipe -- the pipe that bounds this kernel.
-__device__ __forceinline__ uint64_t add64(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.u64 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-
 // One counter forward.  k2x2 = 2*k*k.
 __device__ __forceinline__ void step(State& s, uint64_t k, uint64_t k2x2) {
   s.y = add64(s.y, k);
@@ -110,7 +117,7 @@ __device__ __forceinline__ void step(State& s, uint64_t k, uint64_t k2x2) {
 // Jump by J = 2^LOGJ counters.  jk = J*k, cj = J*(J-1)*k*k, dj = J*2*k*k (all mod 2^64).
 template <int LOGJ>
 __device__ __forceinline__ void jump(State& s, uint64_t jk, uint64_t cj, uint64_t dj) {
-  s.u = add64(s.u, add64(s.e << LOGJ, cj));
+  s.u = add64_3(s.u, s.e << LOGJ, cj);
   s.y = add64(s.y, jk);
   s.e = add64(s.e, dj);
 }

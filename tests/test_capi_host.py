@@ -79,6 +79,10 @@ def test_fill_argument_errors_without_device(sq):
         assert fn(fake_keys, 2, 0, 10, fake_out, 9, None) == sq.SQ_EINVAL    # ld < n
         assert fn(fake_keys, 1, 0, 10, fake_out + 2, 10, None) == sq.SQ_EINVAL  # misaligned
         assert fn(fake_keys, 1 << 40, 0, 1 << 40, fake_out, 1 << 40, None) == sq.SQ_EINVAL  # size
+    for fn in (lib.sq_fill_u32_k, lib.sq_fill_u64_k, lib.sq_fill_f32_k):
+        assert fn(1, 0, 0, None, None) == sq.SQ_OK
+        assert fn(1, 0, 10, None, None) == sq.SQ_EINVAL
+        assert fn(1, 0, 10, fake_out + 2, None) == sq.SQ_EINVAL
     assert lib.sq_fused_stats(1, 0, 0, None, None, None) == sq.SQ_OK
     assert lib.sq_fused_stats(1, 0, 5, None, 0x1000, None) == sq.SQ_EINVAL
     assert lib.sq_fused_stats(1, 0, 5, 0x1004, 0x1000, None) == sq.SQ_EINVAL

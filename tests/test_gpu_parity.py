@@ -75,6 +75,22 @@ def test_fill_edges(sq, kind, edge):
     assert (allbits[:off] == fill_val).all() and (allbits[off + nkeys * ld:] == fill_val).all()
 
 
+@pytest.mark.parametrize("kind", ["u32", "u64", "f32"])
+@pytest.mark.parametrize("ctr0,n", [(0, 1), (7, 33), ((1 << 64) - 1000, 4099), ((1 << 32) - 5, (1 << 20) + 17)])
+def test_fill_by_value_key(sq, kind, ctr0, n):
+    """sq_fill_*_k (key by value, uniform-register constants) vs the oracle, incl. a
+    misaligned output pointer (offset by one element)."""
+    key = int(O.keygen(2, 1)[0])
+    dt = {"u32": torch.int32, "u64": torch.int64, "f32": torch.float32}[kind]
+    buf = torch.zeros(n + 2, dtype=dt, device="cuda")
+    getattr(sq, f"fill_{kind}_k")(key, ctr0, n, out=buf[1:n + 1])
+    torch.cuda.synchronize()
+    got = buf.cpu().numpy().view(VIEW[kind])
+    want = O.fill(kind, [key], ctr0, n)[0].view(VIEW[kind])
+    assert np.array_equal(got[1:n + 1], want), first_mismatch(got[1:n + 1], want)
+    assert got[0] == 0 and got[n + 1] == 0
+
+
 @pytest.mark.parametrize("kind", ["u32", "u64"])
 def test_fill_corner_keys(sq, kind):
     """Kernels are total over (ctr, key): key 0, 1, 2^32, 2^64-1 and random odd/even."""

@@ -1,0 +1,106 @@
+// loopbench.cu -- compute-only throughput of alternative formulations of the squares32 inner
+// loop (no stores: results are XOR-folded), to pick the SASS mix that runs fastest on B200.
+// Not part of the product.  Build:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -o tools/loopbench tools/loopbench.cu
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s line %d\n", cudaGetErrorString(e_), __LINE__); return 1; } } while (0)
+
+__device__ __forceinline__ uint64_t add64(uint64_t a, uint64_t b) { uint64_t d; asm("add.u64 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ uint64_t add64_3(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d; asm("add.u64 %0, %1, %2;\n\tadd.u64 %0, %0, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c)); return d; }
+__device__ __forceinline__ uint32_t shl1(uint32_t x) { uint32_t d; asm("shl.b32 %0, %1, 1;" : "=r"(d) : "r"(x)); return d; }
+
+template <int DBL>
+__device__ __forceinline__ void rr(uint32_t& xh, uint32_t& xl, uint64_t w) {
+  uint64_t t = (uint64_t)xl * xl + w;
+  uint32_t hi;
+  if (DBL == 0) hi = (uint32_t)(t >> 32) + xl * (xh << 1);
+  else if (DBL == 1) hi = (uint32_t)(t >> 32) + xl * shl1(xh);
+  else { uint32_t c = xl * xh; hi = (uint32_t)(t >> 32) + (c << 1); }
+  xh = (uint32_t)t; xl = hi;
+}
+template <int DBL>
+__device__ __forceinline__ uint32_t rh(uint32_t xh, uint32_t xl, uint64_t w) {
+  uint64_t t = (uint64_t)xl * xl + w;
+  if (DBL == 0) return (uint32_t)(t >> 32) + xl * (xh << 1);
+  if (DBL == 1) return (uint32_t)(t >> 32) + xl * shl1(xh);
+  uint32_t c = xl * xh; return (uint32_t)(t >> 32) + (c << 1);
+}
+
+// FORM: 0 = y chain + 3-input u (cst), 1 = y chain + 2-input u/e chains, 2 = y from base + 3-input u
+template <int FORM, int DBL, int SPL>
+__global__ void __launch_bounds__(256) kloop(uint64_t key, uint64_t ctr0, int iters, uint32_t* out) {
+  const uint64_t k2 = 2 * key * key;
+  uint64_t cst[SPL + 1], jk[SPL + 1];
+  cst[0] = 0; jk[0] = 0;
+#pragma unroll
+  for (int j = 1; j <= SPL; j++) { cst[j] = cst[j - 1] + k2; jk[j] = jk[j - 1] + key; }
+  const uint64_t J = 32ull * SPL;
+  const uint64_t c = ctr0 + ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * SPL;
+  uint64_t y0 = c * key, u0 = y0 * y0 + y0, e0 = 2 * key * y0 + key * key + key;
+  const uint64_t JK = J * key, CJ = J * (J - 1) * key * key, DJ = J * k2;
+  uint32_t acc = 0;
+  for (int it = 0; it < iters; it++) {
+    uint64_t y = y0, u = u0, e = e0;
+#pragma unroll
+    for (int j = 0; j < SPL; j++) {
+      uint64_t yy, z;
+      if (FORM == 2) { yy = add64(y0, jk[j]); z = add64(y0, jk[j + 1]); }
+      else { yy = y; z = add64(y, key); }
+      uint32_t xh = (uint32_t)u, xl = (uint32_t)(u >> 32);
+      rr<DBL>(xh, xl, z);
+      rr<DBL>(xh, xl, yy);
+      acc ^= rh<DBL>(xh, xl, z);
+      y = z;
+      if (FORM == 1) { u = add64(u, e); e = add64(e, k2); }
+      else u = add64_3(u, e0, cst[j]);
+    }
+    u0 = add64_3(u0, e0 << (SPL == 8 ? 8 : SPL == 16 ? 9 : 7), CJ);
+    y0 = add64(y0, JK);
+    e0 = add64(e0, DJ);
+  }
+  if (acc == 0x9E3779B9u) out[0] = acc;
+}
+
+template <typename K>
+static int run(K kern, const char* name, int spl) {
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0));
+  int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int blocks = sms * occ;
+  int iters = 4096 / spl * 8;
+  uint32_t* out; CK(cudaMalloc(&out, 4));
+  cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, kern);
+  kern<<<blocks, 256>>>(0x1fac726d8cb5432full, 0, iters, out);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  float best = 1e9;
+  for (int r = 0; r < 5; r++) {
+    cudaEventRecord(a);
+    kern<<<blocks, 256>>>(0x1fac726d8cb5432full, 0, iters, out);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
+  }
+  double samples = (double)blocks * 256 * iters * spl;
+  printf("{\"variant\": \"%s\", \"gsps\": %.1f, \"regs\": %d, \"occ\": %d}\n", name, samples / best / 1e6, fa.numRegs, occ);
+  cudaFree(out);
+  return 0;
+}
+
+int main() {
+  run(kloop<0, 0, 8>, "F0_D0_S8", 8);
+  run(kloop<1, 0, 8>, "F1_D0_S8", 8);
+  run(kloop<2, 0, 8>, "F2_D0_S8", 8);
+  run(kloop<0, 1, 8>, "F0_D1_S8", 8);
+  run(kloop<0, 2, 8>, "F0_D2_S8", 8);
+  run(kloop<2, 2, 8>, "F2_D2_S8", 8);
+  run(kloop<0, 0, 16>, "F0_D0_S16", 16);
+  run(kloop<2, 0, 16>, "F2_D0_S16", 16);
+  run(kloop<0, 2, 16>, "F0_D2_S16", 16);
+  run(kloop<0, 0, 4>, "F0_D0_S4", 4);
+  return 0;
+}

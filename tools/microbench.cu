@@ -18,7 +18,7 @@
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
   fprintf(stderr, "CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); exit(1);} } while (0)
 
-enum Op { OP_IMAD, OP_WIDE, OP_HI, OP_IADD, OP_LOP3, OP_I2F, OP_ROUND, OP_SHL };
+enum Op { OP_IMAD, OP_WIDE, OP_HI, OP_IADD, OP_LOP3, OP_I2F, OP_ROUND, OP_SHL, OP_WIDEF, OP_HI64, OP_IADD64 };
 
 template <int OP>
 __global__ void k_pipe(uint32_t* out, int iters, unsigned long long* cyc) {
@@ -41,6 +41,15 @@ __global__ void k_pipe(uint32_t* out, int iters, unsigned long long* cyc) {
       if (OP == OP_WIDE) {
         uint32_t lo = (uint32_t)w[j], hi = (uint32_t)(w[j] >> 32);
         asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(w[j]) : "r"(lo), "r"(hi ^ (uint32_t)w[j1]));
+      }
+      if (OP == OP_WIDEF) {  // folded 64-bit addend (plain C so ptxas emits IMAD.WIDE.U32 d, a, b, c64)
+        w[j] = (uint64_t)(uint32_t)w[j] * (uint32_t)(w[j1] >> 32) + w[j2];
+      }
+      if (OP == OP_HI64) {   // high word of a*b + c64: IMAD.HI.U32 with a 64-bit addend
+        a[j] = (uint32_t)(((uint64_t)a[j] * a[j1] + w[j]) >> 32);
+      }
+      if (OP == OP_IADD64) { // 64-bit add chain (IADD3 + IADD3.X or IMAD.X)
+        w[j] = w[j] + w[j1];
       }
       if (OP == OP_HI)   asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(a[j]) : "r"(m), "r"(a[j1]));
       if (OP == OP_IADD) asm volatile("add.u32 %0, %0, %1;" : "+r"(a[j]) : "r"(a[j1]));
@@ -263,6 +272,9 @@ int main(int argc, char** argv) {
   run_pipe(k_pipe<OP_IMAD>, "IMAD", 8, 256, 8, it, 0, nullptr, false);
   run_pipe(k_pipe<OP_WIDE>, "IMAD.WIDE.U32", 8, 256, 8, it, 0, nullptr, false);
   run_pipe(k_pipe<OP_HI>, "IMAD.HI.U32", 8, 256, 8, it, 0, nullptr, false);
+  run_pipe(k_pipe<OP_WIDEF>, "IMAD.WIDE.U32.folded64", 8, 256, 8, it, 0, nullptr, false);
+  run_pipe(k_pipe<OP_HI64>, "IMAD.HI.U32.addend64", 8, 256, 8, it, 0, nullptr, false);
+  run_pipe(k_pipe<OP_IADD64>, "IADD64", 8, 256, 8, it, 0, nullptr, false);
   run_pipe(k_pipe<OP_IADD>, "IADD", 8, 256, 8, it, 0, nullptr, false);
   run_pipe(k_pipe<OP_LOP3>, "LOP3", 8, 256, 8, it, 0, nullptr, false);
   run_pipe(k_pipe<OP_SHL>, "SHL", 8, 256, 8, it, 0, nullptr, false);

@@ -16,17 +16,21 @@ for l in body.split("\n"):
     if m:
         ins.append((int(m.group(1), 16), m.group(2).strip()))
 addr_idx = {a: i for i, (a, _) in enumerate(ins)}
-mi = next(i for i, (_, s) in enumerate(ins) if marker in s)
-# innermost backward branch that jumps to <= marker and sits after it
+mis = [i for i, (_, s) in enumerate(ins) if marker in s]
+# innermost backward branch whose loop body contains a marker instruction
 best = None
 for i, (a, s) in enumerate(ins):
-    m = re.search(r"BRA\s+(?:`\()?.*?0x([0-9a-f]+)", s)
-    if m and i > mi:
-        tgt = int(m.group(1), 16)
-        if tgt in addr_idx and addr_idx[tgt] <= mi:
-            if best is None or (i - addr_idx[tgt]) < (best[1] - best[0]):
-                best = (addr_idx[tgt], i)
-lo, hi = best
+    m = re.search(r"BRA(?:\.U)?\s+(?:!?U?P\w+,\s*)?(?:`\()?.*?0x([0-9a-f]+)", s)
+    if not m:
+        continue
+    tgt = int(m.group(1), 16)
+    if tgt not in addr_idx or addr_idx[tgt] >= i:
+        continue
+    lo_i = addr_idx[tgt]
+    nmark = sum(1 for mi in mis if lo_i <= mi <= i)
+    if nmark and (best is None or (i - lo_i) < (best[1] - best[0])):
+        best = (lo_i, i, nmark)
+lo, hi, nmark = best
 ops = []
 for _, s in ins[lo:hi + 1]:
     s = re.sub(r"^@!?U?P\w+\s+", "", s)
@@ -36,4 +40,4 @@ fma = sum(v * (2 if (k.startswith("IMAD.WIDE") or k.startswith("IMAD.HI")) else 
 alu = sum(v for k, v in c.items() if k.split(".")[0] in ("IADD3", "LOP3", "SHF", "SEL", "ISETP", "MOV", "LEA", "PRMT", "VIADD", "POPC", "FLO", "I2FP"))
 for k, v in c.most_common():
     print(f"{v:5d} {k}")
-print(f"loop [{lo},{hi}] instructions={hi-lo+1} fma_slots(WIDE/HI=2)={fma} alu~={alu}")
+print(f"loop [{lo},{hi}] instructions={hi-lo+1} markers={nmark} fma_slots(WIDE/HI=2)={fma} alu~={alu}")
