@@ -43,7 +43,18 @@ struct FusedShared {
   uint32_t* fix;                  // 16: fix-ups of bins with bit j set
 };
 
-__device__ __noinline__ void guard_fixup(uint32_t* bins, uint32_t b, uint32_t inc,
+#ifndef SQ_FUSED_INLINE_FIX
+#define SQ_FUSED_INLINE_FIX 0
+#endif
+#ifndef SQ_FUSED_INC_SHIFT
+#define SQ_FUSED_INC_SHIFT 0
+#endif
+#if SQ_FUSED_INLINE_FIX
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+void guard_fixup(uint32_t* bins, uint32_t b, uint32_t inc,
                                          unsigned long long* hist, uint32_t* fix) {
   atomicSub(&bins[b >> 1], inc << 15);                 // half -= 0x8000
   atomicAdd(&hist[b], 0x8000ull);
@@ -55,7 +66,11 @@ __device__ __noinline__ void guard_fixup(uint32_t* bins, uint32_t b, uint32_t in
 __device__ __forceinline__ void hist_add(uint32_t* bins, uint32_t u, unsigned long long* hist,
                                          uint32_t* fix) {
   const uint32_t b = u >> 16;
+#if SQ_FUSED_INC_SHIFT
+  const uint32_t inc = 1u << ((u >> 12) & 16u);
+#else
   const uint32_t inc = (u & 0x10000u) ? 0x10000u : 1u;
+#endif
   const uint32_t old = atomicAdd(&bins[b >> 1], inc);
   if (((old + inc) ^ old) & 0x80008000u) guard_fixup(bins, b, inc, hist, fix);
 }

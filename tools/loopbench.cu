@@ -13,26 +13,36 @@ __device__ __forceinline__ uint64_t add64_3(uint64_t a, uint64_t b, uint64_t c) 
   uint64_t d; asm("add.u64 %0, %1, %2;\n\tadd.u64 %0, %0, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c)); return d; }
 __device__ __forceinline__ uint32_t shl1(uint32_t x) { uint32_t d; asm("shl.b32 %0, %1, 1;" : "=r"(d) : "r"(x)); return d; }
 
+__device__ uint32_t g_zr;   // unused; zr comes from a kernel parameter
 template <int DBL>
-__device__ __forceinline__ void rr(uint32_t& xh, uint32_t& xl, uint64_t w) {
+__device__ __forceinline__ uint32_t dbl(uint32_t x, uint32_t zr) {
+  uint32_t d;
+  if (DBL == 3) asm("add.u32 %0, %1, %1;\n\tadd.u32 %0, %0, %2;" : "=r"(d) : "r"(x), "r"(zr));
+  else asm("shf.l.clamp.b32 %0, %2, %1, 1;" : "=r"(d) : "r"(x), "r"(zr));
+  return d;
+}
+template <int DBL>
+__device__ __forceinline__ void rr(uint32_t& xh, uint32_t& xl, uint64_t w, uint32_t zr) {
   uint64_t t = (uint64_t)xl * xl + w;
   uint32_t hi;
   if (DBL == 0) hi = (uint32_t)(t >> 32) + xl * (xh << 1);
   else if (DBL == 1) hi = (uint32_t)(t >> 32) + xl * shl1(xh);
-  else { uint32_t c = xl * xh; hi = (uint32_t)(t >> 32) + (c << 1); }
+  else if (DBL == 2) { uint32_t c = xl * xh; hi = (uint32_t)(t >> 32) + (c << 1); }
+  else hi = (uint32_t)(t >> 32) + xl * dbl<DBL>(xh, zr);
   xh = (uint32_t)t; xl = hi;
 }
 template <int DBL>
-__device__ __forceinline__ uint32_t rh(uint32_t xh, uint32_t xl, uint64_t w) {
+__device__ __forceinline__ uint32_t rh(uint32_t xh, uint32_t xl, uint64_t w, uint32_t zr) {
   uint64_t t = (uint64_t)xl * xl + w;
   if (DBL == 0) return (uint32_t)(t >> 32) + xl * (xh << 1);
   if (DBL == 1) return (uint32_t)(t >> 32) + xl * shl1(xh);
-  uint32_t c = xl * xh; return (uint32_t)(t >> 32) + (c << 1);
+  if (DBL == 2) { uint32_t c = xl * xh; return (uint32_t)(t >> 32) + (c << 1); }
+  return (uint32_t)(t >> 32) + xl * dbl<DBL>(xh, zr);
 }
 
 // FORM: 0 = y chain + 3-input u (cst), 1 = y chain + 2-input u/e chains, 2 = y from base + 3-input u
 template <int FORM, int DBL, int SPL>
-__global__ void __launch_bounds__(256) kloop(uint64_t key, uint64_t ctr0, int iters, uint32_t* out) {
+__global__ void __launch_bounds__(256) kloop(uint64_t key, uint64_t ctr0, int iters, uint32_t* out, uint32_t zr) {
   const uint64_t k2 = 2 * key * key;
   uint64_t cst[SPL + 1], jk[SPL + 1];
   cst[0] = 0; jk[0] = 0;
@@ -51,9 +61,9 @@ __global__ void __launch_bounds__(256) kloop(uint64_t key, uint64_t ctr0, int it
       if (FORM == 2) { yy = add64(y0, jk[j]); z = add64(y0, jk[j + 1]); }
       else { yy = y; z = add64(y, key); }
       uint32_t xh = (uint32_t)u, xl = (uint32_t)(u >> 32);
-      rr<DBL>(xh, xl, z);
-      rr<DBL>(xh, xl, yy);
-      acc ^= rh<DBL>(xh, xl, z);
+      rr<DBL>(xh, xl, z, zr);
+      rr<DBL>(xh, xl, yy, zr);
+      acc ^= rh<DBL>(xh, xl, z, zr);
       y = z;
       if (FORM == 1) { u = add64(u, e); e = add64(e, k2); }
       else u = add64_3(u, e0, cst[j]);
@@ -74,13 +84,13 @@ static int run(K kern, const char* name, int spl) {
   int iters = 4096 / spl * 8;
   uint32_t* out; CK(cudaMalloc(&out, 4));
   cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, kern);
-  kern<<<blocks, 256>>>(0x1fac726d8cb5432full, 0, iters, out);
+  kern<<<blocks, 256>>>(0x1fac726d8cb5432full, 0, iters, out, 0u);
   CK(cudaDeviceSynchronize());
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   float best = 1e9;
   for (int r = 0; r < 5; r++) {
     cudaEventRecord(a);
-    kern<<<blocks, 256>>>(0x1fac726d8cb5432full, 0, iters, out);
+    kern<<<blocks, 256>>>(0x1fac726d8cb5432full, 0, iters, out, 0u);
     cudaEventRecord(b);
     CK(cudaEventSynchronize(b));
     float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
@@ -92,6 +102,10 @@ static int run(K kern, const char* name, int spl) {
 }
 
 int main() {
+  run(kloop<0, 3, 16>, "F0_D3_S16", 16);
+  run(kloop<0, 4, 16>, "F0_D4_S16", 16);
+  run(kloop<0, 3, 8>, "F0_D3_S8", 8);
+  run(kloop<0, 4, 8>, "F0_D4_S8", 8);
   run(kloop<0, 0, 8>, "F0_D0_S8", 8);
   run(kloop<1, 0, 8>, "F1_D0_S8", 8);
   run(kloop<2, 0, 8>, "F2_D0_S8", 8);

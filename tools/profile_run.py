@@ -33,7 +33,10 @@ def main():
         dt = {"u32": torch.int32, "u64": torch.int64, "f32": torch.float32}[w.kind]
         out = torch.empty((w.nkeys, n), dtype=dt, device="cuda")
         for _ in range(a.reps):
-            getattr(sq, f"fill_{w.kind}")(keys, w.ctr0, n, out=out)
+            if w.nkeys == 1:   # same entry point as bench.py: key by value
+                getattr(sq, f"fill_{w.kind}_k")(int(keys[0]), w.ctr0, n, out=out.view(-1))
+            else:
+                getattr(sq, f"fill_{w.kind}")(keys, w.ctr0, n, out=out)
     torch.cuda.synchronize()
     print("ok", a.workload, n)
 
