@@ -121,6 +121,48 @@ int sq_fill_u64_k(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* out_dev, sq
 int sq_fill_f32_k(uint64_t key, uint64_t ctr0, uint64_t n, float* out_dev, sq_stream_t stream);
 
 /* ----------------------------------------------------------------------------------------
+ * Output kinds and the generic fill (squares64-derived floats, strided
+ * counters).  Kinds:
+ *   SQ_KIND_U32    squares32, uint32                                  4 bytes
+ *   SQ_KIND_U64    squares64, uint64                                  8 bytes
+ *   SQ_KIND_F32    (float)(squares32 >> 8) * 2^-24 in [0,1)  (BASELINE.json config 4)   4 bytes
+ *   SQ_KIND_F64    (double)(squares64 >> 11) * 2^-53 in [0,1) ("53-bit precision floating
+ *                  point"; formula S:260), exact                          8 bytes
+ *   SQ_KIND_F32X2  squares64 split into two 32-bit halves, each (h >> 8) * 2^-24, LOW half
+ *                  first ("splits the 64 bits into two 32-bit halves"; order S:269).
+ *                  One element = a pair of floats (8 bytes): n counters give 2n floats and
+ *                  `ld` counts pairs.
+ * All conversions are exact (no rounding): the integer fits the float's significand and the
+ * scale is a power of two.
+ * -------------------------------------------------------------------------------------- */
+#define SQ_KIND_U32 0
+#define SQ_KIND_U64 1
+#define SQ_KIND_F32 2
+#define SQ_KIND_F64 3
+#define SQ_KIND_F32X2 4
+
+int sq_fill_f64(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n,
+                double* out_dev, uint64_t ld, sq_stream_t stream);
+int sq_fill_f32x2(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n,
+                  float* out_dev, uint64_t ld, sq_stream_t stream);
+int sq_fill_f64_k(uint64_t key, uint64_t ctr0, uint64_t n, double* out_dev, sq_stream_t stream);
+int sq_fill_f32x2_k(uint64_t key, uint64_t ctr0, uint64_t n, float* out_dev, sq_stream_t stream);
+
+/* Generic fill: out[k*ld + i] = G_kind(ctr0 + i*stride mod 2^64, key_k) where key_k =
+ * keys_dev[k] (k < nkeys), or, when keys_dev is NULL, the single key `key_imm` (nkeys must
+ * be 1).  stride = 1 is the consecutive walk of the fills above; stride > 1 evaluates "counter
+ * tests with increments other than one".  stride = 0 is rejected (SQ_EINVAL:
+ * use sq_fill_keyctr for a fixed counter).  Other errors as for sq_fill_u32. */
+int sq_fill_ex(int kind, const uint64_t* keys_dev, uint64_t nkeys, uint64_t key_imm, uint64_t ctr0,
+               uint64_t stride, uint64_t n, void* out_dev, uint64_t ld, sq_stream_t stream);
+
+/* Key-counter mode ("the counter was fixed and only the key changed"):
+ * out[j] = G_kind(ctr, keys_dev[j]) for j < nkeys, densely packed (element size of `kind`).
+ * nkeys == 0 is SQ_OK without a launch; NULL pointers or a misaligned out_dev: SQ_EINVAL. */
+int sq_fill_keyctr(int kind, const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr, void* out_dev,
+                   sq_stream_t stream);
+
+/* ----------------------------------------------------------------------------------------
  * Fused generate-and-reduce (BASELINE.json config 5; the GPU analogue of P:45's "basic
  * uniformity test").  With u_i = squares32(ctr0 + i mod 2^64, key), i < n, ACCUMULATES
  *   hist_dev[b] += #{i : u_i >> 16 == b}            b < 65536
@@ -133,6 +175,14 @@ int sq_fill_f32_k(uint64_t key, uint64_t ctr0, uint64_t n, float* out_dev, sq_st
 int sq_fused_stats(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist_dev,
                    uint64_t* ones_dev, sq_stream_t stream);
 
+/* Fused statistics over the strided counters ctr0 + i*stride (i < n; stride >= 1) with an
+ * optional output transform: flags & SQ_FUSED_BITREV counts bitrev32(u_i) instead of u_i
+ * ("bits-reversed tests"), i.e. hist over the reversed low 16 bits.
+ * stride = 0 or unknown flag bits: SQ_EINVAL. */
+#define SQ_FUSED_BITREV 1u
+int sq_fused_stats_ex(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
+                      uint64_t* hist_dev, uint64_t* ones_dev, sq_stream_t stream);
+
 /* ----------------------------------------------------------------------------------------
  * Host-buffer fill (the end-to-end path): the same map as sq_fill_u32 / sq_fill_u64 /
  * sq_fill_f32 for ONE key, written to HOST memory.  The library generates chunks of
@@ -141,7 +191,7 @@ int sq_fused_stats(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist_dev,
  * overlapping generation of chunk c+1 with the copy of chunk c via `copy_stream`.  The call is
  * SYNCHRONOUS: it returns after out_host holds all n elements.  out_host should be pinned
  * (cudaHostAlloc / cudaHostRegister) for full PCIe bandwidth.
- *   kind        0 = u32, 1 = u64, 2 = f32
+ *   kind        SQ_KIND_* (0 = u32, 1 = u64, 2 = f32, 3 = f64, 4 = f32x2)
  *   key         the key (host value)
  *   scratch_dev device scratch, >= 2 * 32 bytes, 256-byte aligned recommended
  * Errors: SQ_EINVAL (bad kind, NULL pointers with n > 0, scratch too small), SQ_ECUDA.

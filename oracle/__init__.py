@@ -61,6 +61,13 @@ def lib() -> ctypes.CDLL:
                 "oracle_fill_f32": (None, [P, u64, u64, u64, P, u64]),
                 "oracle_f32_from_u32": (ctypes.c_float, [u32]),
                 "oracle_fused_stats": (None, [u64, u64, u64, P, P]),
+                "oracle_f64_from_u64": (ctypes.c_double, [u64]),
+                "oracle_fill_f64": (None, [P, u64, u64, u64, P, u64]),
+                "oracle_fill_f32x2": (None, [P, u64, u64, u64, P, u64]),
+                "oracle_fill_strided": (None, [ctypes.c_int, P, u64, u64, u64, u64, P, u64]),
+                "oracle_fill_keyctr": (None, [ctypes.c_int, P, u64, u64, P]),
+                "oracle_bitrev32": (u32, [u32]),
+                "oracle_fused_stats_ex": (None, [u64, u64, u64, u64, ctypes.c_int, P, P]),
                 "oracle_xorfold_u32": (u64, [u64, u64, u64]),
                 "oracle_weyl_check": (ctypes.c_int, [u64, u64]),
                 "oracle_validate_key": (u32, [u64]),
@@ -141,14 +148,51 @@ def _keys_array(keys) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(keys, dtype=np.uint64).reshape(-1))
 
 
+KIND_CODE = {"u32": 0, "u64": 1, "f32": 2, "f64": 3, "f32x2": 4}
+KIND_DTYPE = {"u32": np.uint32, "u64": np.uint64, "f32": np.float32, "f64": np.float64, "f32x2": np.float32}
+
+
 def fill(kind: str, keys, ctr0: int, n: int, ld: int | None = None) -> np.ndarray:
-    """out[k, i] = G(ctr0 + i mod 2^64, keys[k]) for kind in u32 | u64 | f32; shape (nkeys, ld)."""
+    """out[k, i] = G(ctr0 + i mod 2^64, keys[k]) for kind in u32 | u64 | f32 | f64 | f32x2;
+    shape (nkeys, ld) (f32x2: (nkeys, ld, 2), low half first)."""
     ka = _keys_array(keys)
     ld = n if ld is None else ld
-    dt = {"u32": np.uint32, "u64": np.uint64, "f32": np.float32}[kind]
-    out = np.zeros((ka.size, ld), dtype=dt)
+    shape = (ka.size, ld, 2) if kind == "f32x2" else (ka.size, ld)
+    out = np.zeros(shape, dtype=KIND_DTYPE[kind])
     getattr(lib(), f"oracle_fill_{kind}")(_ptr(ka), ka.size, ctr0 & M64, n, _ptr(out), ld)
     return out
+
+
+def fill_strided(kind: str, keys, ctr0: int, stride: int, n: int, ld: int | None = None) -> np.ndarray:
+    """Raw element bits (uint32 for u32/f32, uint64 otherwise) of the strided fill."""
+    ka = _keys_array(keys)
+    ld = n if ld is None else ld
+    out = np.zeros((ka.size, ld), dtype=np.uint32 if kind in ("u32", "f32") else np.uint64)
+    lib().oracle_fill_strided(KIND_CODE[kind], _ptr(ka), ka.size, ctr0 & M64, stride & M64, n, _ptr(out), ld)
+    return out
+
+
+def fill_keyctr(kind: str, keys, ctr: int) -> np.ndarray:
+    """Raw element bits of G(ctr, keys[j]) for every key j (key-counter mode)."""
+    ka = _keys_array(keys)
+    out = np.zeros(ka.size, dtype=np.uint32 if kind in ("u32", "f32") else np.uint64)
+    lib().oracle_fill_keyctr(KIND_CODE[kind], _ptr(ka), ka.size, ctr & M64, _ptr(out))
+    return out
+
+
+def f64_from_u64(v: int) -> float:
+    return lib().oracle_f64_from_u64(v & M64)
+
+
+def bitrev32(u: int) -> int:
+    return lib().oracle_bitrev32(u & 0xFFFFFFFF)
+
+
+def fused_stats_ex(key: int, ctr0: int, stride: int, n: int, bitrev: bool = False):
+    hist = np.zeros(65536, dtype=np.uint64)
+    ones = np.zeros(32, dtype=np.uint64)
+    lib().oracle_fused_stats_ex(key & M64, ctr0 & M64, stride & M64, n, int(bitrev), _ptr(hist), _ptr(ones))
+    return hist, ones
 
 
 def f32_from_u32(u: int) -> float:

@@ -183,6 +183,91 @@ void oracle_fused_stats(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist,
   }
 }
 
+/* ------------------------------------------------------------------------------------ */
+/* squares64-derived floats ("53-bit precision floating point" and "splits the 64 bits */
+/* into two 32-bit halves"; formulas S:260 and S:269).                                      */
+/* ------------------------------------------------------------------------------------ */
+
+/* (v >> 11) * 2^-53: exact (a 53-bit integer times a power of two). */
+double oracle_f64_from_u64(uint64_t v) { return (double)(v >> 11) * 0x1p-53; }
+
+void oracle_fill_f64(const uint64_t* keys, uint64_t nkeys, uint64_t ctr0, uint64_t n,
+                     double* out, uint64_t ld) {
+  for (uint64_t k = 0; k < nkeys; k++)
+    for (uint64_t i = 0; i < n; i++)
+      out[k * ld + i] = oracle_f64_from_u64(oracle_squares64(ctr0 + i, keys[k]));
+}
+
+/* Two floats per squares64 output, low half first; ld counts float PAIRS. */
+void oracle_fill_f32x2(const uint64_t* keys, uint64_t nkeys, uint64_t ctr0, uint64_t n,
+                       float* out, uint64_t ld) {
+  for (uint64_t k = 0; k < nkeys; k++)
+    for (uint64_t i = 0; i < n; i++) {
+      uint64_t v = oracle_squares64(ctr0 + i, keys[k]);
+      out[2 * (k * ld + i)] = oracle_f32_from_u32((uint32_t)v);
+      out[2 * (k * ld + i) + 1] = oracle_f32_from_u32((uint32_t)(v >> 32));
+    }
+}
+
+/* One output of kind 0..4 (u32, u64, f32, f64, f32x2) for counter c, as 8 raw bytes
+ * (4-byte kinds in the low word). */
+static uint64_t oracle_one(int kind, uint64_t c, uint64_t key) {
+  union { float f; uint32_t u; } a, b;
+  union { double d; uint64_t u; } dd;
+  switch (kind) {
+    case 0: return oracle_squares32(c, key);
+    case 1: return oracle_squares64(c, key);
+    case 2: a.f = oracle_f32_from_u32(oracle_squares32(c, key)); return a.u;
+    case 3: dd.d = oracle_f64_from_u64(oracle_squares64(c, key)); return dd.u;
+    default: {
+      uint64_t v = oracle_squares64(c, key);
+      a.f = oracle_f32_from_u32((uint32_t)v);
+      b.f = oracle_f32_from_u32((uint32_t)(v >> 32));
+      return ((uint64_t)b.u << 32) | a.u;
+    }
+  }
+}
+
+/* Strided counters ("counter tests with increments other than one"):
+ * element i of row k uses counter ctr0 + i*stride mod 2^64.  out is raw bytes of the kind's
+ * element size (4 for u32/f32, 8 otherwise); ld in elements. */
+void oracle_fill_strided(int kind, const uint64_t* keys, uint64_t nkeys, uint64_t ctr0, uint64_t stride,
+                         uint64_t n, void* out, uint64_t ld) {
+  for (uint64_t k = 0; k < nkeys; k++)
+    for (uint64_t i = 0; i < n; i++) {
+      uint64_t v = oracle_one(kind, ctr0 + i * stride, keys[k]);
+      if (kind == 0 || kind == 2) ((uint32_t*)out)[k * ld + i] = (uint32_t)v;
+      else ((uint64_t*)out)[k * ld + i] = v;
+    }
+}
+
+/* Key-counter mode ("the counter was fixed and only the key changed"). */
+void oracle_fill_keyctr(int kind, const uint64_t* keys, uint64_t nkeys, uint64_t ctr, void* out) {
+  for (uint64_t j = 0; j < nkeys; j++) {
+    uint64_t v = oracle_one(kind, ctr, keys[j]);
+    if (kind == 0 || kind == 2) ((uint32_t*)out)[j] = (uint32_t)v;
+    else ((uint64_t*)out)[j] = v;
+  }
+}
+
+/* Bit reversal of a 32-bit word ("bits-reversed tests"), bit by bit. */
+uint32_t oracle_bitrev32(uint32_t u) {
+  uint32_t r = 0;
+  for (int j = 0; j < 32; j++) r |= ((u >> j) & 1u) << (31 - j);
+  return r;
+}
+
+/* Fused statistics over strided counters, optionally of the bit-reversed outputs. */
+void oracle_fused_stats_ex(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, int bitrev,
+                           uint64_t* hist, uint64_t* ones) {
+  for (uint64_t i = 0; i < n; i++) {
+    uint32_t u = oracle_squares32(ctr0 + i * stride, key);
+    if (bitrev) u = oracle_bitrev32(u);
+    hist[u >> 16] += 1;
+    for (int j = 0; j < 32; j++) ones[j] += (u >> j) & 1u;
+  }
+}
+
 /* XOR-fold of a u32 fill with no output buffer: the CPU-baseline timing kernel
  * ("dead-code-elimination guard").  Same per-counter definition as oracle_fill_u32. */
 uint64_t oracle_xorfold_u32(uint64_t key, uint64_t ctr0, uint64_t n) {

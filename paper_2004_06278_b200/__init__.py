@@ -24,7 +24,8 @@ LIB_PATH = os.path.join(_HERE, "libsquares.so")
 
 SQ_OK, SQ_EINVAL, SQ_ERANGE, SQ_ECUDA, SQ_ENOMEM = 0, 1, 2, 3, 4
 KEY_UPPER_REPEAT, KEY_LOWER_REPEAT, KEY_ZERO_DIGIT, KEY_EVEN, KEY_POPCOUNT = 1, 2, 4, 8, 16
-KINDS = {"u32": 0, "u64": 1, "f32": 2}
+KINDS = {"u32": 0, "u64": 1, "f32": 2, "f64": 3, "f32x2": 4}
+SQ_FUSED_BITREV = 1
 HIST_BINS = 65536
 M64 = (1 << 64) - 1
 
@@ -63,7 +64,14 @@ def _load() -> ctypes.CDLL:
         "sq_fill_u32_k": (i32, [u64, u64, u64, vp, vp]),
         "sq_fill_u64_k": (i32, [u64, u64, u64, vp, vp]),
         "sq_fill_f32_k": (i32, [u64, u64, u64, vp, vp]),
+        "sq_fill_f64": (i32, [vp, u64, u64, u64, vp, u64, vp]),
+        "sq_fill_f32x2": (i32, [vp, u64, u64, u64, vp, u64, vp]),
+        "sq_fill_f64_k": (i32, [u64, u64, u64, vp, vp]),
+        "sq_fill_f32x2_k": (i32, [u64, u64, u64, vp, vp]),
+        "sq_fill_ex": (i32, [i32, vp, u64, u64, u64, u64, u64, vp, u64, vp]),
+        "sq_fill_keyctr": (i32, [i32, vp, u64, u64, vp, vp]),
         "sq_fused_stats": (i32, [u64, u64, u64, vp, vp, vp]),
+        "sq_fused_stats_ex": (i32, [u64, u64, u64, u64, u32, vp, vp, vp]),
         "sq_fill_host": (i32, [i32, u64, u64, u64, vp, vp, ctypes.c_size_t, vp, vp]),
     }
     for name, (res, args) in sigs.items():
@@ -76,7 +84,8 @@ def _load() -> ctypes.CDLL:
 
 EXPORTED_SYMBOLS = ("sq_strerror", "sq_last_cuda_error", "sq_version", "sq_validate_key", "sq_keygen",
                     "sq_fill_u32", "sq_fill_u64", "sq_fill_f32", "sq_fill_u32_k", "sq_fill_u64_k",
-                    "sq_fill_f32_k", "sq_fused_stats", "sq_fill_host")
+                    "sq_fill_f32_k", "sq_fill_f64", "sq_fill_f32x2", "sq_fill_f64_k", "sq_fill_f32x2_k", "sq_fill_ex", "sq_fill_keyctr",
+                    "sq_fused_stats", "sq_fused_stats_ex", "sq_fill_host")
 
 
 def _check(fn: str, code: int) -> None:
@@ -112,7 +121,21 @@ def keygen(seed: int, count: int) -> torch.Tensor:
 
 
 # ----------------------------------------------------------------------------- device functions
-_OUT_DTYPE = {"u32": torch.int32, "u64": torch.int64, "f32": torch.float32}
+# element dtypes; an f32x2 element is a PAIR of float32 (low half of squares64 first), so its
+# tensors have a trailing dimension of 2.
+_OUT_DTYPE = {"u32": torch.int32, "u64": torch.int64, "f32": torch.float32, "f64": torch.float64,
+              "f32x2": torch.float32}
+_ELEM_BYTES = {"u32": 4, "u64": 8, "f32": 4, "f64": 8, "f32x2": 8}
+
+
+def _alloc(kind, shape, device):
+    if kind == "f32x2":
+        shape = tuple(shape) + (2,)
+    return torch.empty(shape, dtype=_OUT_DTYPE[kind], device=device)
+
+
+def _elems(kind, t: torch.Tensor) -> int:
+    return t.numel() * t.element_size() // _ELEM_BYTES[kind]
 
 
 def _fill(kind: str, keys: torch.Tensor, ctr0: int, n: int, out: torch.Tensor | None, ld: int | None,
@@ -122,14 +145,15 @@ def _fill(kind: str, keys: torch.Tensor, ctr0: int, n: int, out: torch.Tensor | 
     nkeys = keys.numel()
     if out is None:
         ld = n if ld is None else ld
-        out = torch.empty((nkeys, ld), dtype=_OUT_DTYPE[kind], device=keys.device)
+        out = _alloc(kind, (nkeys, ld), keys.device)
     else:
         if out.dtype != _OUT_DTYPE[kind] or not out.is_cuda:
             raise ValueError(f"out must be a CUDA {_OUT_DTYPE[kind]} tensor")
         if ld is None:
-            ld = out.shape[-1] if out.dim() == 2 else n
+            nd = 3 if kind == "f32x2" else 2
+            ld = out.shape[1] if out.dim() == nd else n
         need = (nkeys - 1) * ld + n if nkeys else 0
-        if out.numel() - 0 < need or not out.is_contiguous():
+        if _elems(kind, out) < need or not out.is_contiguous():
             raise ValueError("out is too small or not contiguous")
     fn = getattr(_load(), f"sq_fill_{kind}")
     _check(f"sq_fill_{kind}", fn(keys.data_ptr(), nkeys, _u64(ctr0), int(n), out.data_ptr(), int(ld),
@@ -140,8 +164,8 @@ def _fill(kind: str, keys: torch.Tensor, ctr0: int, n: int, out: torch.Tensor | 
 def _fill_k(kind: str, key: int, ctr0: int, n: int, out: torch.Tensor | None, device=None,
             stream=None) -> torch.Tensor:
     if out is None:
-        out = torch.empty(int(n), dtype=_OUT_DTYPE[kind], device=device if device is not None else "cuda")
-    elif out.dtype != _OUT_DTYPE[kind] or not out.is_cuda or not out.is_contiguous() or out.numel() < n:
+        out = _alloc(kind, (int(n),), device if device is not None else "cuda")
+    elif out.dtype != _OUT_DTYPE[kind] or not out.is_cuda or not out.is_contiguous() or _elems(kind, out) < n:
         raise ValueError(f"out must be a contiguous CUDA {_OUT_DTYPE[kind]} tensor of >= n elements")
     fn = getattr(_load(), f"sq_fill_{kind}_k")
     _check(f"sq_fill_{kind}_k", fn(_u64(key), _u64(ctr0), int(n), out.data_ptr(), _stream_handle(stream)))
@@ -178,6 +202,75 @@ def fill_f32(keys, ctr0, n, out=None, ld=None, stream=None):
     return _fill("f32", keys, ctr0, n, out, ld, stream)
 
 
+def fill_f64(keys, ctr0, n, out=None, ld=None, stream=None):
+    """out[k, i] = (squares64(ctr0 + i, keys[k]) >> 11) * 2^-53, float64 in [0, 1) (P:67)."""
+    return _fill("f64", keys, ctr0, n, out, ld, stream)
+
+
+def fill_f32x2(keys, ctr0, n, out=None, ld=None, stream=None):
+    """out[k, i, :] = the two 32-bit halves of squares64(ctr0 + i, keys[k]) as floats
+    (h >> 8) * 2^-24, low half first."""
+    return _fill("f32x2", keys, ctr0, n, out, ld, stream)
+
+
+def fill_f64_k(key, ctr0, n, out=None, device=None, stream=None):
+    return _fill_k("f64", key, ctr0, n, out, device, stream)
+
+
+def fill_f32x2_k(key, ctr0, n, out=None, device=None, stream=None):
+    return _fill_k("f32x2", key, ctr0, n, out, device, stream)
+
+
+def fill_ex(kind: str, ctr0: int, n: int, stride: int = 1, keys: torch.Tensor | None = None,
+            key: int | None = None, out: torch.Tensor | None = None, ld: int | None = None,
+            device=None, stream=None) -> torch.Tensor:
+    """Generic fill (sq_fill_ex): counters ctr0 + i*stride; either a device keys tensor
+    (rows) or one key by value."""
+    if (keys is None) == (key is None):
+        raise ValueError("pass exactly one of keys (device tensor) or key (int)")
+    if keys is not None:
+        if not (keys.is_cuda and keys.dtype == torch.int64 and keys.dim() == 1 and keys.is_contiguous()):
+            raise ValueError("keys must be a contiguous 1-D int64 CUDA tensor")
+        nkeys, kptr, kimm, dev = keys.numel(), keys.data_ptr(), 0, keys.device
+    else:
+        nkeys, kptr, kimm, dev = 1, None, _u64(key), (device if device is not None else "cuda")
+    ld = n if ld is None else ld
+    if out is None:
+        out = _alloc(kind, (nkeys, ld), dev)
+    elif out.dtype != _OUT_DTYPE[kind] or not out.is_cuda or not out.is_contiguous() or \
+            _elems(kind, out) < (nkeys - 1) * ld + n:
+        raise ValueError("bad out tensor")
+    _check("sq_fill_ex", _load().sq_fill_ex(KINDS[kind], kptr, nkeys, kimm, _u64(ctr0), _u64(stride), int(n),
+                                            out.data_ptr(), int(ld), _stream_handle(stream)))
+    return out
+
+
+def fill_keyctr(kind: str, keys: torch.Tensor, ctr: int, out: torch.Tensor | None = None, stream=None):
+    """Key-counter mode: out[j] = G(ctr, keys[j])."""
+    if not (keys.is_cuda and keys.dtype == torch.int64 and keys.dim() == 1 and keys.is_contiguous()):
+        raise ValueError("keys must be a contiguous 1-D int64 CUDA tensor")
+    if out is None:
+        out = _alloc(kind, (keys.numel(),), keys.device)
+    elif out.dtype != _OUT_DTYPE[kind] or not out.is_cuda or not out.is_contiguous() or \
+            _elems(kind, out) < keys.numel():
+        raise ValueError("bad out tensor")
+    _check("sq_fill_keyctr", _load().sq_fill_keyctr(KINDS[kind], keys.data_ptr(), keys.numel(), _u64(ctr),
+                                                    out.data_ptr(), _stream_handle(stream)))
+    return out
+
+
+def fused_stats_ex(key: int, ctr0: int, n: int, stride: int = 1, bitrev: bool = False,
+                   hist: torch.Tensor | None = None, ones: torch.Tensor | None = None, device=None, stream=None):
+    """Fused statistics over counters ctr0 + i*stride, optionally of bit-reversed outputs."""
+    dev = device if device is not None else (hist.device if hist is not None else torch.device("cuda"))
+    hist = torch.zeros(HIST_BINS, dtype=torch.int64, device=dev) if hist is None else hist
+    ones = torch.zeros(32, dtype=torch.int64, device=dev) if ones is None else ones
+    _check("sq_fused_stats_ex", _load().sq_fused_stats_ex(_u64(key), _u64(ctr0), _u64(stride), int(n),
+                                                          SQ_FUSED_BITREV if bitrev else 0, hist.data_ptr(),
+                                                          ones.data_ptr(), _stream_handle(stream)))
+    return hist, ones
+
+
 def fused_stats(key: int, ctr0: int, n: int, hist: torch.Tensor | None = None,
                 ones: torch.Tensor | None = None, device=None, stream=None):
     """Accumulate the top-16-bit histogram (65536 bins) and the 32 per-bit ones counts of
@@ -199,7 +292,7 @@ def fill_host(kind: str, key: int, ctr0: int, n: int, out_host: torch.Tensor, sc
               stream=None, copy_stream=None) -> torch.Tensor:
     """End-to-end fill of ONE key into a (pinned) host tensor via the library's chunked
     generate + D2H pipeline.  Synchronous."""
-    es = 8 if kind == "u64" else 4
+    es = _ELEM_BYTES[kind]
     if out_host.is_cuda or out_host.numel() * out_host.element_size() < n * es:
         raise ValueError("out_host must be a host tensor of at least n elements")
     if not scratch.is_cuda:

@@ -13,7 +13,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsquares.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["capi.cu", "fill.cu", "fused.cu", "keygen.cpp"]
+SOURCES = ["capi.cu", "fill.cu", "fused.cu", "keyctr.cu", "keygen.cpp"]
 HEADERS = ["squares_device.cuh", "sq_internal.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v"]
@@ -29,18 +29,18 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None, extra=()) -> str:
     """Compile libsquares.so (or, for experiments, a variant with extra -D defines at `out`)."""
     lib = out or LIB
-    if not force and not defines and out is None and not _stale():
+    if not force and not defines and not extra and out is None and not _stale():
         return LIB
-    tag = "_".join(d.replace("=", "") for d in defines) or "default"
+    tag = "_".join([d.replace("=", "") for d in defines] + [e.strip("-").replace(" ", "") for e in extra]) or "default"
     objdir = os.path.join(PKG, "build", tag)
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

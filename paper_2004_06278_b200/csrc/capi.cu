@@ -46,23 +46,35 @@ static bool size_ok(uint64_t nkeys, uint64_t ld, uint64_t es) {
   return bytes <= (unsigned __int128)SIZE_MAX;
 }
 
-static int fill_entry(int kind, const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n,
-                      void* out_dev, uint64_t ld, cudaStream_t stream) {
-  const uint64_t es = (kind == KIND_U64) ? 8 : 4;
+static bool kind_ok(int kind) { return kind >= KIND_U32 && kind <= KIND_F32X2; }
+
+// keys_dev == nullptr: single row with key key_imm (nkeys must be 1).
+static int fill_any(int kind, const uint64_t* keys_dev, uint64_t nkeys, uint64_t key_imm, uint64_t ctr0,
+                    uint64_t stride, uint64_t n, void* out_dev, uint64_t ld, cudaStream_t stream) {
+  if (!kind_ok(kind) || stride == 0) return SQ_EINVAL;
+  const uint64_t es = kind_elem_bytes(kind);
   if (n == 0 || nkeys == 0) return SQ_OK;
-  if (!keys_dev || !out_dev) return SQ_EINVAL;
+  if (!out_dev) return SQ_EINVAL;
+  if (!keys_dev && nkeys != 1) return SQ_EINVAL;
   if (((uintptr_t)out_dev % es) != 0) return SQ_EINVAL;
   if (nkeys == 1) ld = n;
   if (ld < n) return SQ_EINVAL;
   if (!size_ok(nkeys, ld, es)) return SQ_EINVAL;
   FillArgs a{};
   a.keys = keys_dev;
-  a.key_imm = 0;
+  a.key_imm = key_imm;
   a.ctr0 = ctr0;
+  a.stride = stride;
   a.n = n;
   a.out = (char*)out_dev;
   a.ld_bytes = ld * es;
   return launch_fill_kind(kind, a, nkeys, n, stream);
+}
+
+static int fill_entry(int kind, const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n,
+                      void* out_dev, uint64_t ld, cudaStream_t stream) {
+  if (n != 0 && nkeys != 0 && !keys_dev) return SQ_EINVAL;
+  return fill_any(kind, keys_dev, nkeys, 0, ctr0, 1, n, out_dev, ld, stream);
 }
 
 }  // namespace sq
@@ -84,7 +96,7 @@ const char* sq_strerror(int code) {
 
 int sq_last_cuda_error(void) { return g_last_cuda_error; }
 
-int sq_version(void) { return 100; }
+int sq_version(void) { return 200; }
 
 int sq_fill_u32(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n, uint32_t* out_dev,
                 uint64_t ld, sq_stream_t stream) {
@@ -102,19 +114,7 @@ int sq_fill_f32(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_
 }
 
 static int fill_key_entry(int kind, uint64_t key, uint64_t ctr0, uint64_t n, void* out_dev, cudaStream_t stream) {
-  const uint64_t es = (kind == KIND_U64) ? 8 : 4;
-  if (n == 0) return SQ_OK;
-  if (!out_dev) return SQ_EINVAL;
-  if (((uintptr_t)out_dev % es) != 0) return SQ_EINVAL;
-  if (!size_ok(1, n, es)) return SQ_EINVAL;
-  FillArgs a{};
-  a.keys = nullptr;
-  a.key_imm = key;
-  a.ctr0 = ctr0;
-  a.n = n;
-  a.out = (char*)out_dev;
-  a.ld_bytes = n * es;
-  return launch_fill_kind(kind, a, 1, n, stream);
+  return fill_any(kind, nullptr, 1, key, ctr0, 1, n, out_dev, n, stream);
 }
 
 int sq_fill_u32_k(uint64_t key, uint64_t ctr0, uint64_t n, uint32_t* out_dev, sq_stream_t stream) {
@@ -129,20 +129,59 @@ int sq_fill_f32_k(uint64_t key, uint64_t ctr0, uint64_t n, float* out_dev, sq_st
   return fill_key_entry(KIND_F32, key, ctr0, n, out_dev, (cudaStream_t)stream);
 }
 
-int sq_fused_stats(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist_dev, uint64_t* ones_dev,
+int sq_fill_f64(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n, double* out_dev,
+                uint64_t ld, sq_stream_t stream) {
+  return fill_entry(KIND_F64, keys_dev, nkeys, ctr0, n, out_dev, ld, (cudaStream_t)stream);
+}
+
+int sq_fill_f32x2(const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr0, uint64_t n, float* out_dev,
+                  uint64_t ld, sq_stream_t stream) {
+  return fill_entry(KIND_F32X2, keys_dev, nkeys, ctr0, n, out_dev, ld, (cudaStream_t)stream);
+}
+
+int sq_fill_f64_k(uint64_t key, uint64_t ctr0, uint64_t n, double* out_dev, sq_stream_t stream) {
+  return fill_key_entry(KIND_F64, key, ctr0, n, out_dev, (cudaStream_t)stream);
+}
+
+int sq_fill_f32x2_k(uint64_t key, uint64_t ctr0, uint64_t n, float* out_dev, sq_stream_t stream) {
+  return fill_key_entry(KIND_F32X2, key, ctr0, n, out_dev, (cudaStream_t)stream);
+}
+
+int sq_fill_ex(int kind, const uint64_t* keys_dev, uint64_t nkeys, uint64_t key_imm, uint64_t ctr0,
+               uint64_t stride, uint64_t n, void* out_dev, uint64_t ld, sq_stream_t stream) {
+  return fill_any(kind, keys_dev, nkeys, key_imm, ctr0, stride, n, out_dev, ld, (cudaStream_t)stream);
+}
+
+int sq_fill_keyctr(int kind, const uint64_t* keys_dev, uint64_t nkeys, uint64_t ctr, void* out_dev,
                    sq_stream_t stream) {
+  if (!kind_ok(kind)) return SQ_EINVAL;
+  if (nkeys == 0) return SQ_OK;
+  if (!keys_dev || !out_dev) return SQ_EINVAL;
+  if (((uintptr_t)out_dev % kind_elem_bytes(kind)) != 0 || ((uintptr_t)keys_dev & 7)) return SQ_EINVAL;
+  if (!size_ok(1, nkeys, 8)) return SQ_EINVAL;
+  return launch_keyctr(kind, keys_dev, nkeys, ctr, out_dev, (cudaStream_t)stream);
+}
+
+int sq_fused_stats_ex(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
+                      uint64_t* hist_dev, uint64_t* ones_dev, sq_stream_t stream) {
+  if (stride == 0 || (flags & ~SQ_FUSED_BITREV)) return SQ_EINVAL;
   if (n == 0) return SQ_OK;
   if (!hist_dev || !ones_dev) return SQ_EINVAL;
   if (((uintptr_t)hist_dev & 7) || ((uintptr_t)ones_dev & 7)) return SQ_EINVAL;
-  return launch_fused(key, ctr0, n, hist_dev, ones_dev, (cudaStream_t)stream);
+  return launch_fused(key, ctr0, stride, n, flags, hist_dev, ones_dev, (cudaStream_t)stream);
+}
+
+int sq_fused_stats(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist_dev, uint64_t* ones_dev,
+                   sq_stream_t stream) {
+  return sq_fused_stats_ex(key, ctr0, 1, n, 0, hist_dev, ones_dev, stream);
 }
 
 int sq_fill_host(int kind, uint64_t key, uint64_t ctr0, uint64_t n, void* out_host, void* scratch_dev,
                  size_t scratch_bytes, sq_stream_t stream, sq_stream_t copy_stream) {
-  if (kind != KIND_U32 && kind != KIND_U64 && kind != KIND_F32) return SQ_EINVAL;
+  if (!kind_ok(kind)) return SQ_EINVAL;
   if (n == 0) return SQ_OK;
   if (!out_host || !scratch_dev) return SQ_EINVAL;
-  const uint64_t es = (kind == KIND_U64) ? 8 : 4;
+  const uint64_t es = kind_elem_bytes(kind);
   // two ping-pong halves, each a multiple of 32 bytes
   const uint64_t half = (scratch_bytes / 2) & ~(uint64_t)31;
   const uint64_t chunk = half / es;
@@ -169,6 +208,7 @@ int sq_fill_host(int kind, uint64_t key, uint64_t ctr0, uint64_t n, void* out_ho
     a.keys = nullptr;
     a.key_imm = key;
     a.ctr0 = ctr0 + done;
+    a.stride = 1;
     a.n = m;
     a.out = buf;
     a.ld_bytes = m * es;

@@ -20,14 +20,13 @@
 namespace sq {
 
 template <int KIND>
-struct FillTraits;
-template <>
-struct FillTraits<KIND_U32> { static constexpr int ES = 4, SPL = 16, LOGJ = 9; };
-template <>
-struct FillTraits<KIND_F32> { static constexpr int ES = 4, SPL = 16, LOGJ = 9; };
-template <>
-struct FillTraits<KIND_U64> { static constexpr int ES = 8, SPL = 8, LOGJ = 8; };
-// SPL = samples per lane per chunk (64 bytes: two 256-bit stores); J = 32 * SPL = 2^LOGJ.
+struct FillTraits {
+  // ES = element bytes; SPL = samples per lane per chunk (64 bytes per lane = two 256-bit
+  // stores); J = 32 * SPL counters per warp chunk = 2^LOGJ.
+  static constexpr int ES = kind_elem_bytes(KIND);
+  static constexpr int SPL = 64 / ES;
+  static constexpr int LOGJ = (SPL == 16) ? 9 : 8;
+};
 
 __device__ __forceinline__ void st256(void* p, const uint32_t* v) {
   asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]),
@@ -35,22 +34,25 @@ __device__ __forceinline__ void st256(void* p, const uint32_t* v) {
                : "memory");
 }
 
-// Per-row constants of the counter walk (squares_device.cuh): key, the chunk jump
-// (J*k, J(J-1)k^2, 2Jk^2) and cst[j] = j*2k^2 for the in-chunk 3-input u step.
+// Per-row constants of the counter walk (squares_device.cuh): the key, the stepping
+// increment K = stride*key, the chunk jump (J*K, J(J-1)K^2, 2JK^2) and cst[j] = j*2K^2 for
+// the in-chunk 3-input u step.
 template <int SPL>
 struct RowConst {
-  uint64_t key, jk, cj, dj;
+  uint64_t key, K, jk, cj, dj;
   uint64_t cst[SPL];
 };
 
 template <int SPL>
-__device__ __forceinline__ RowConst<SPL> row_const(uint64_t key) {
+__device__ __forceinline__ RowConst<SPL> row_const(uint64_t key, uint64_t stride) {
   constexpr uint64_t J = 32 * SPL;
   RowConst<SPL> rc;
-  const uint64_t k2x2 = 2 * key * key;
+  const uint64_t K = stride * key;
+  const uint64_t k2x2 = 2 * K * K;
   rc.key = key;
-  rc.jk = J * key;
-  rc.cj = J * (J - 1) * key * key;
+  rc.K = K;
+  rc.jk = J * K;
+  rc.cj = J * (J - 1) * K * K;
   rc.dj = J * k2x2;
   rc.cst[0] = 0;
 #pragma unroll
@@ -58,24 +60,40 @@ __device__ __forceinline__ RowConst<SPL> row_const(uint64_t key) {
   return rc;
 }
 
-// The SPL consecutive outputs of one lane from state s (not modified), packed as 32-bit words
-// (u64 outputs little-endian: low word first).
-template <int KIND, int SPL>
+// Output words of one sample j of kind KIND into v (little-endian 64-bit elements).
+template <int KIND>
+__device__ __forceinline__ void put(uint32_t (&v)[16], int j, uint64_t y, uint64_t z, uint64_t u) {
+  if (KIND == KIND_U32 || KIND == KIND_F32) {
+    const uint32_t o = squares32_from(y, z, u);
+    v[j] = (KIND == KIND_F32) ? __float_as_uint(u32_to_unit_f32(o)) : o;
+  } else {
+    const uint64_t o = squares64_from(y, z, u);
+    if (KIND == KIND_U64) {
+      v[2 * j] = lo32(o);
+      v[2 * j + 1] = hi32(o);
+    } else if (KIND == KIND_F64) {
+      const uint64_t d = (uint64_t)__double_as_longlong(u64_to_unit_f64(o));
+      v[2 * j] = lo32(d);
+      v[2 * j + 1] = hi32(d);
+    } else {  // KIND_F32X2: low half first, then high half
+      v[2 * j] = __float_as_uint(u32_to_unit_f32(lo32(o)));
+      v[2 * j + 1] = __float_as_uint(u32_to_unit_f32(hi32(o)));
+    }
+  }
+}
+
+// The SPL outputs of one lane from state s (not modified).  Consecutive counters
+// (STRIDED = false): z = y + key is the next counter's y.  Strided: y steps by K and
+// z = y + key separately (one more 64-bit add per sample).
+template <int KIND, int SPL, bool STRIDED>
 __device__ __forceinline__ void gen_lane(const State& s, const RowConst<SPL>& rc, uint32_t (&v)[16]) {
   uint64_t y = s.y, u = s.u;
 #pragma unroll
   for (int j = 0; j < SPL; j++) {
-    const uint64_t z = add64(y, rc.key);        // z = (c+1)*key = next counter's y
-    if (KIND == KIND_U64) {
-      const uint64_t o = squares64_from(y, z, u);
-      v[2 * j] = lo32(o);
-      v[2 * j + 1] = hi32(o);
-    } else {
-      const uint32_t o = squares32_from(y, z, u);
-      v[j] = (KIND == KIND_F32) ? __float_as_uint(u32_to_unit_f32(o)) : o;
-    }
+    const uint64_t z = add64(y, rc.key);
+    put<KIND>(v, j, y, z, u);
     if (j < SPL - 1) {
-      y = z;
+      y = STRIDED ? add64(y, rc.K) : z;
       u = j ? add64_3(u, s.e, rc.cst[j]) : add64(u, s.e);
     }
   }
@@ -83,14 +101,13 @@ __device__ __forceinline__ void gen_lane(const State& s, const RowConst<SPL>& rc
 
 // KEYIMM: a single row whose key is a kernel parameter, so ptxas can keep the key and the
 // per-row constants in uniform registers (sq_fill_*_k).  Otherwise keys[row] from memory.
-template <int KIND, bool KEYIMM>
+template <int KIND, bool KEYIMM, bool STRIDED>
 __global__ void __launch_bounds__(kFillThreads, kFillMinBlocks) fill_kernel(FillArgs a) {
   constexpr int ES = FillTraits<KIND>::ES;
   constexpr int SPL = FillTraits<KIND>::SPL;
   constexpr int LOGJ = FillTraits<KIND>::LOGJ;
   constexpr int J = 32 * SPL;            // counters per warp chunk
-  constexpr int LANE_BYTES = SPL * ES;   // 64
-  static_assert((1 << LOGJ) == J && LANE_BYTES == 64, "chunk geometry");
+  static_assert((1 << LOGJ) == J && SPL * ES == 64, "chunk geometry");
 
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warps_per_cta = blockDim.x >> 5;
@@ -105,7 +122,8 @@ __global__ void __launch_bounds__(kFillThreads, kFillMinBlocks) fill_kernel(Fill
   uint32_t nostore_acc = 0;
 #endif
   while (c < c_end) {
-    const RowConst<SPL> rc = row_const<SPL>(KEYIMM ? a.key_imm : __ldg(a.keys + row));
+    const RowConst<SPL> rc =
+        row_const<SPL>(KEYIMM ? a.key_imm : __ldg(a.keys + row), STRIDED ? a.stride : 1);
     char* rowp = a.out + row * a.ld_bytes;
     const uint64_t m = ((uintptr_t)rowp & 31) / ES;      // row misalignment in elements
     uint64_t run = a.chunks_per_row - cc;
@@ -116,7 +134,8 @@ __global__ void __launch_bounds__(kFillThreads, kFillMinBlocks) fill_kernel(Fill
     const uint64_t full_hi = (a.n + m) / J;
     // element index of this lane's first element in chunk cc ("negative" wraps mod 2^64)
     uint64_t i0 = cc * J + lane * SPL - m;
-    State s = state_at(a.ctr0 + i0, rc.key);
+    State s = STRIDED ? state_at_strided(a.ctr0 + i0 * a.stride, rc.key, rc.K)
+                      : state_at(a.ctr0 + i0, rc.key);
     while (cc < cc_stop) {
       uint32_t v[16];
       if (cc >= full_lo && cc < full_hi) {
@@ -126,7 +145,7 @@ __global__ void __launch_bounds__(kFillThreads, kFillMinBlocks) fill_kernel(Fill
         i0 += nfull * J;
         cc += nfull;
         for (; nfull; nfull--) {
-          gen_lane<KIND, SPL>(s, rc, v);
+          gen_lane<KIND, SPL, STRIDED>(s, rc, v);
 #ifdef SQ_FILL_NOSTORE   // experiment: generation without the output stream
 #pragma unroll
           for (int j = 0; j < 16; j++) nostore_acc ^= v[j];
@@ -139,7 +158,7 @@ __global__ void __launch_bounds__(kFillThreads, kFillMinBlocks) fill_kernel(Fill
         }
       } else {
         // boundary chunk (row head or ragged tail): per-element masked stores
-        gen_lane<KIND, SPL>(s, rc, v);
+        gen_lane<KIND, SPL, STRIDED>(s, rc, v);
         char* p = rowp + (int64_t)i0 * ES;
 #pragma unroll
         for (int j = 0; j < SPL; j++) {
@@ -178,7 +197,9 @@ static int launch_fill(const FillArgs& a0, uint64_t nkeys, uint64_t n, cudaStrea
   int occ = 0;
   const DeviceInfo* di = device_info();
   if (!di) return SQ_ECUDA;
-  auto kern = a.keys ? fill_kernel<KIND, false> : fill_kernel<KIND, true>;
+  void (*kern)(FillArgs);
+  if (a.stride == 1) kern = a.keys ? fill_kernel<KIND, false, false> : fill_kernel<KIND, true, false>;
+  else kern = a.keys ? fill_kernel<KIND, false, true> : fill_kernel<KIND, true, true>;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFillThreads, 0);
   if (e != cudaSuccess) return set_cuda_error(e);
   if (occ < 1) occ = 1;
@@ -200,6 +221,8 @@ int launch_fill_kind(int kind, const FillArgs& a, uint64_t nkeys, uint64_t n, cu
     case KIND_U32: return launch_fill<KIND_U32>(a, nkeys, n, stream);
     case KIND_U64: return launch_fill<KIND_U64>(a, nkeys, n, stream);
     case KIND_F32: return launch_fill<KIND_F32>(a, nkeys, n, stream);
+    case KIND_F64: return launch_fill<KIND_F64>(a, nkeys, n, stream);
+    case KIND_F32X2: return launch_fill<KIND_F32X2>(a, nkeys, n, stream);
     default: return SQ_EINVAL;
   }
 }

@@ -97,22 +97,27 @@ __device__ __forceinline__ void warp_flush16(uint32_t (&cnt)[16], unsigned long 
   }
 }
 
-// Per-key constants of the counter walk: cst[j] = j*2k^2 (j < 8), cst8 = 8*2k^2.
+// Per-key constants of the counter walk: K = stride*key (the y step), cst[j] = j*2K^2 (j < 8),
+// cst8 = 8*2K^2.
 struct WalkConst {
-  uint64_t key;
+  uint64_t key, K;
   uint64_t cst[8];
   uint64_t cst8;
 };
 
 // 8 consecutive samples from state s; s advances by 8 counters.  u uses the 3-input step
 // u(c+j+1) = u(c+j) + e(c) + j*2k^2 (squares_device.cuh), e advances once per group.
+// STRIDED: counters advance by `stride` (y by K, z = y + key separately); BITREV: each
+// output is bit-reversed before it is counted ("bits-reversed tests").
+template <bool STRIDED, bool BITREV>
 __device__ __forceinline__ void gen8(State& s, const WalkConst& wc, uint32_t (&v)[8]) {
   uint64_t y = s.y, u = s.u;
 #pragma unroll
   for (int j = 0; j < 8; j++) {
     const uint64_t z = add64(y, wc.key);
-    v[j] = squares32_from(y, z, u);
-    y = z;
+    const uint32_t o = squares32_from(y, z, u);
+    v[j] = BITREV ? __brev(o) : o;
+    y = STRIDED ? add64(y, wc.K) : z;
     u = j ? add64_3(u, s.e, wc.cst[j]) : add64(u, s.e);
   }
   s.y = y;
@@ -140,7 +145,7 @@ __device__ __forceinline__ void reduce8(const uint32_t (&v)[8], uint32_t (&w)[4]
 }
 
 // One epoch (32 samples = 16 packed words) folded by Harley-Seal into a weight-16 word.
-template <bool MASKED>
+template <bool MASKED, bool STRIDED, bool BITREV>
 __device__ __forceinline__ uint32_t epoch(State& s, const WalkConst& wc, uint32_t* bins,
                                           unsigned long long* hist, uint32_t* fix, int64_t rem,
                                           uint32_t& ones, uint32_t& twos, uint32_t& fours,
@@ -152,7 +157,7 @@ __device__ __forceinline__ uint32_t epoch(State& s, const WalkConst& wc, uint32_
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       uint32_t v[8], w[4], twosA, twosB;
-      gen8(s, wc, v);
+      gen8<STRIDED, BITREV>(s, wc, v);
       reduce8<MASKED>(v, w, bins, hist, fix, rem - 8 * (2 * blk + h));
       csa(twosA, ones, ones, w[0], w[1]);
       csa(twosB, ones, ones, w[2], w[3]);
@@ -165,8 +170,9 @@ __device__ __forceinline__ uint32_t epoch(State& s, const WalkConst& wc, uint32_
   return sixteens;
 }
 
+template <bool STRIDED, bool BITREV>
 __global__ void __launch_bounds__(kFusedThreads, 1)
-fused_kernel(uint64_t key, uint64_t ctr0, uint64_t q, uint64_t r, uint32_t epochs,
+fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t r, uint32_t epochs,
              unsigned long long* __restrict__ hist, unsigned long long* __restrict__ ones_out) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* bins = smem;
@@ -181,11 +187,13 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t q, uint64_t r, uint32_t epoch
   const uint64_t t = (uint64_t)blockIdx.x * kFusedThreads + tid;
   const uint64_t start = t * q + (t < r ? t : r);
   const uint64_t cnt = q + (t < r ? 1 : 0);
-  State s = state_at(ctr0 + start, key);
+  const uint64_t K = STRIDED ? stride * key : key;
+  State s = STRIDED ? state_at_strided(ctr0 + start * stride, key, K) : state_at(ctr0 + start, key);
   WalkConst wc;
   {
-    const uint64_t k2x2 = 2 * key * key;
+    const uint64_t k2x2 = 2 * K * K;
     wc.key = key;
+    wc.K = K;
     wc.cst[0] = 0;
 #pragma unroll
     for (int j = 1; j < 8; j++) wc.cst[j] = wc.cst[j - 1] + k2x2;
@@ -205,10 +213,10 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t q, uint64_t r, uint32_t epoch
   for (uint32_t ep = 0; ep < epochs; ep++) {
     uint32_t sixteens;
     if (done + kEpoch <= cnt) {
-      sixteens = epoch<false>(s, wc, bins, hist, fix, kEpoch, ones, twos, fours, eights);
+      sixteens = epoch<false, STRIDED, BITREV>(s, wc, bins, hist, fix, kEpoch, ones, twos, fours, eights);
     } else {
       const int64_t rem = done < cnt ? (int64_t)(cnt - done) : 0;
-      sixteens = epoch<true>(s, wc, bins, hist, fix, rem, ones, twos, fours, eights);
+      sixteens = epoch<true, STRIDED, BITREV>(s, wc, bins, hist, fix, rem, ones, twos, fours, eights);
     }
     done += kEpoch;
     // ripple-add the weight-16 word into the vertical planes
@@ -266,12 +274,15 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t q, uint64_t r, uint32_t epoch
   }
 }
 
-int launch_fused(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist, uint64_t* ones,
-                 cudaStream_t stream) {
+int launch_fused(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
+                 uint64_t* hist, uint64_t* ones, cudaStream_t stream) {
   const DeviceInfo* di = device_info();
   if (!di) return SQ_ECUDA;
-  cudaError_t e = cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)kFusedSmem);
+  const bool strided = stride != 1, bitrev = (flags & SQ_FUSED_BITREV) != 0;
+  decltype(&fused_kernel<false, false>) kern =
+      strided ? (bitrev ? fused_kernel<true, true> : fused_kernel<true, false>)
+              : (bitrev ? fused_kernel<false, true> : fused_kernel<false, false>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFusedSmem);
   if (e != cudaSuccess) return set_cuda_error(e);
   // one CTA per SM; small n uses fewer CTAs (>= 2^20 samples each) so the flush amortises
   uint64_t blocks = (n + (1ull << 20) - 1) >> 20;
@@ -282,8 +293,8 @@ int launch_fused(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist, uint64
   const uint64_t per = q + (r ? 1 : 0);
   const uint64_t epochs = (per + kEpoch - 1) / kEpoch;
   if (epochs > 0xFFFFFFFFull) return SQ_ERANGE;
-  fused_kernel<<<(unsigned)blocks, kFusedThreads, kFusedSmem, stream>>>(
-      key, ctr0, q, r, (uint32_t)epochs, (unsigned long long*)hist, (unsigned long long*)ones);
+  kern<<<(unsigned)blocks, kFusedThreads, kFusedSmem, stream>>>(
+      key, ctr0, stride, q, r, (uint32_t)epochs, (unsigned long long*)hist, (unsigned long long*)ones);
   return set_cuda_error(cudaGetLastError());
 }
 

@@ -7,7 +7,10 @@
 
 namespace sq {
 
-enum Kind { KIND_U32 = 0, KIND_U64 = 1, KIND_F32 = 2 };
+// Output kinds (the numeric values are the C ABI's SQ_KIND_* constants).
+enum Kind { KIND_U32 = 0, KIND_U64 = 1, KIND_F32 = 2, KIND_F64 = 3, KIND_F32X2 = 4 };
+
+__host__ __device__ constexpr int kind_elem_bytes(int kind) { return (kind == KIND_U32 || kind == KIND_F32) ? 4 : 8; }
 
 #ifndef SQ_FILL_THREADS
 #define SQ_FILL_THREADS 256
@@ -23,6 +26,7 @@ struct FillArgs {
   const uint64_t* keys;     // device keys, or nullptr to use key_imm (single row)
   uint64_t key_imm;
   uint64_t ctr0;
+  uint64_t stride;          // counter increment between consecutive outputs (1 = consecutive)
   uint64_t n;
   char* out;                // row 0 base
   uint64_t ld_bytes;        // row pitch in bytes
@@ -44,7 +48,10 @@ int set_cuda_error(cudaError_t e);
 
 int launch_fill_kind(int kind, const FillArgs& a, uint64_t nkeys, uint64_t n, cudaStream_t stream);
 
-int launch_fused(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist, uint64_t* ones,
-                 cudaStream_t stream);
+int launch_fused(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
+                 uint64_t* hist, uint64_t* ones, cudaStream_t stream);
+
+int launch_keyctr(int kind, const uint64_t* keys, uint64_t nkeys, uint64_t ctr, void* out,
+                  cudaStream_t stream);
 
 }  // namespace sq

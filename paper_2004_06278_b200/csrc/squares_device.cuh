@@ -107,6 +107,17 @@ __device__ __forceinline__ State state_at(uint64_t c, uint64_t k) {
   return s;
 }
 
+// Strided walk (counter c, c + stride, c + 2*stride, ...): y steps by K = stride*k, so
+// u(i+1) - u(i) = 2*K*y(i) + K^2 + K and the second difference is 2*K^2.  (z = y + k still
+// uses the key itself.)
+__device__ __forceinline__ State state_at_strided(uint64_t c, uint64_t k, uint64_t K) {
+  State s;
+  s.y = c * k;
+  s.u = s.y * s.y + s.y;
+  s.e = 2 * K * s.y + K * K + K;
+  return s;
+}
+
 // One counter forward.  k2x2 = 2*k*k.
 __device__ __forceinline__ void step(State& s, uint64_t k, uint64_t k2x2) {
   s.y = add64(s.y, k);
@@ -125,6 +136,11 @@ __device__ __forceinline__ void jump(State& s, uint64_t jk, uint64_t cj, uint64_
 // (u >> 8) * 2^-24: top 24 bits of u as a float in [0, 1).  Exact (BASELINE.json config 4).
 __device__ __forceinline__ float u32_to_unit_f32(uint32_t u) {
   return __uint2float_rn(u >> 8) * 0x1p-24f;
+}
+
+// (v >> 11) * 2^-53: top 53 bits of a squares64 output as a double in [0, 1).  Exact.
+__device__ __forceinline__ double u64_to_unit_f64(uint64_t v) {
+  return __ull2double_rn(v >> 11) * 0x1p-53;
 }
 
 }  // namespace sq
