@@ -25,6 +25,7 @@ def _stale() -> bool:
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(os.path.dirname(PKG), "include", "squares.h"))
+    deps.append(os.path.join(os.path.dirname(PKG), "include", "squares_dev.cuh"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps)
 
@@ -56,6 +57,25 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
         raise RuntimeError("link of libsquares.so failed")
     os.replace(tmp, lib)
     return lib
+
+
+DEVTEST_SRC = os.path.join(os.path.dirname(PKG), "tests", "devapi_kernels.cu")
+DEVTEST_LIB = os.path.join(os.path.dirname(PKG), "tests", "libdevapi_test.so")
+
+
+def build_devapi_test(force: bool = False) -> str:
+    """Test kernels that exercise the header-only device API (include/squares_dev.cuh)."""
+    hdr = os.path.join(os.path.dirname(PKG), "include", "squares_dev.cuh")
+    if (not force and os.path.exists(DEVTEST_LIB)
+            and os.path.getmtime(DEVTEST_LIB) > max(os.path.getmtime(DEVTEST_SRC), os.path.getmtime(hdr))):
+        return DEVTEST_LIB
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+           "-o", DEVTEST_LIB, DEVTEST_SRC]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed on tests/devapi_kernels.cu")
+    return DEVTEST_LIB
 
 
 if __name__ == "__main__":
