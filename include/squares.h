@@ -183,6 +183,14 @@ int sq_fused_stats(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist_dev,
 int sq_fused_stats_ex(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
                       uint64_t* hist_dev, uint64_t* ones_dev, sq_stream_t stream);
 
+/* Bit transitions of the output stream, for the runs statistic of the desk battery:
+ * with u_i = squares32(ctr0 + i*stride, key) (bit-reversed if flags & SQ_FUSED_BITREV) read
+ * least-significant bit first, ACCUMULATES into *count_dev (uint64, 8-byte aligned)
+ *   sum_i popc((u_i ^ (u_i >> 1)) & 0x7FFFFFFF) + sum_{0<i<n} [bit31(u_{i-1}) != bit0(u_i)],
+ * i.e. (number of runs) - 1 of the 32n-bit stream.  Errors as for sq_fused_stats_ex. */
+int sq_transitions(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
+                   uint64_t* count_dev, sq_stream_t stream);
+
 /* ----------------------------------------------------------------------------------------
  * Host-buffer fill (the end-to-end path): the same map as sq_fill_u32 / sq_fill_u64 /
  * sq_fill_f32 for ONE key, written to HOST memory.  The library generates chunks of

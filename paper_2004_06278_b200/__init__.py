@@ -72,6 +72,7 @@ def _load() -> ctypes.CDLL:
         "sq_fill_keyctr": (i32, [i32, vp, u64, u64, vp, vp]),
         "sq_fused_stats": (i32, [u64, u64, u64, vp, vp, vp]),
         "sq_fused_stats_ex": (i32, [u64, u64, u64, u64, u32, vp, vp, vp]),
+        "sq_transitions": (i32, [u64, u64, u64, u64, u32, vp, vp]),
         "sq_fill_host": (i32, [i32, u64, u64, u64, vp, vp, ctypes.c_size_t, vp, vp]),
     }
     for name, (res, args) in sigs.items():
@@ -85,7 +86,7 @@ def _load() -> ctypes.CDLL:
 EXPORTED_SYMBOLS = ("sq_strerror", "sq_last_cuda_error", "sq_version", "sq_validate_key", "sq_keygen",
                     "sq_fill_u32", "sq_fill_u64", "sq_fill_f32", "sq_fill_u32_k", "sq_fill_u64_k",
                     "sq_fill_f32_k", "sq_fill_f64", "sq_fill_f32x2", "sq_fill_f64_k", "sq_fill_f32x2_k", "sq_fill_ex", "sq_fill_keyctr",
-                    "sq_fused_stats", "sq_fused_stats_ex", "sq_fill_host")
+                    "sq_fused_stats", "sq_fused_stats_ex", "sq_transitions", "sq_fill_host")
 
 
 def _check(fn: str, code: int) -> None:
@@ -269,6 +270,17 @@ def fused_stats_ex(key: int, ctr0: int, n: int, stride: int = 1, bitrev: bool = 
                                                           SQ_FUSED_BITREV if bitrev else 0, hist.data_ptr(),
                                                           ones.data_ptr(), _stream_handle(stream)))
     return hist, ones
+
+
+def transitions(key: int, ctr0: int, n: int, stride: int = 1, bitrev: bool = False,
+                count: torch.Tensor | None = None, device=None, stream=None) -> torch.Tensor:
+    """Accumulate the number of adjacent differing bits of the LSB-first output bit stream."""
+    dev = device if device is not None else (count.device if count is not None else torch.device("cuda"))
+    count = torch.zeros(1, dtype=torch.int64, device=dev) if count is None else count
+    _check("sq_transitions", _load().sq_transitions(_u64(key), _u64(ctr0), _u64(stride), int(n),
+                                                    SQ_FUSED_BITREV if bitrev else 0, count.data_ptr(),
+                                                    _stream_handle(stream)))
+    return count
 
 
 def fused_stats(key: int, ctr0: int, n: int, hist: torch.Tensor | None = None,

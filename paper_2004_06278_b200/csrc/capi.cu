@@ -171,6 +171,14 @@ int sq_fused_stats_ex(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, 
   return launch_fused(key, ctr0, stride, n, flags, hist_dev, ones_dev, (cudaStream_t)stream);
 }
 
+int sq_transitions(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
+                   uint64_t* count_dev, sq_stream_t stream) {
+  if (stride == 0 || (flags & ~SQ_FUSED_BITREV)) return SQ_EINVAL;
+  if (n == 0) return SQ_OK;
+  if (!count_dev || ((uintptr_t)count_dev & 7)) return SQ_EINVAL;
+  return launch_transitions(key, ctr0, stride, n, flags, count_dev, (cudaStream_t)stream);
+}
+
 int sq_fused_stats(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist_dev, uint64_t* ones_dev,
                    sq_stream_t stream) {
   return sq_fused_stats_ex(key, ctr0, 1, n, 0, hist_dev, ones_dev, stream);

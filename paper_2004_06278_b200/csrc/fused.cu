@@ -299,3 +299,67 @@ int launch_fused(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint3
 }
 
 }  // namespace sq
+
+// ---------------------------------------------------------------------------------------
+// Bit transitions of the output stream (for the runs statistic of the desk battery,
+// SURVEY.md 8(f)3).  The stream is the outputs u_0, u_1, ... of counters
+// ctr0 + i*stride, each read least-significant bit first; transitions = #{adjacent bit pairs
+// that differ} = sum_i popc((u_i ^ (u_i >> 1)) & 0x7FFFFFFF) + sum_{i>0} (bit31(u_{i-1}) != bit0(u_i)).
+// Each thread walks one contiguous index range and also evaluates the sample before it (one
+// extra sample per thread) for the boundary pair.  Accumulates into *count.
+namespace sq {
+
+template <bool STRIDED, bool BITREV>
+__global__ void __launch_bounds__(256)
+transitions_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint64_t q, uint64_t r,
+                   unsigned long long* __restrict__ count) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t start = t * q + (t < r ? t : r);
+  const uint64_t cnt = q + (t < r ? 1 : 0);
+  const uint64_t K = STRIDED ? stride * key : key;
+  uint64_t acc = 0;
+  if (cnt) {
+    State s = STRIDED ? state_at_strided(ctr0 + start * stride, key, K) : state_at(ctr0 + start, key);
+    const uint64_t k2x2 = 2 * K * K;
+    uint32_t prev_bit31 = 0;
+    if (start > 0) {   // boundary with the previous thread's last sample
+      const uint64_t cp = STRIDED ? ctr0 + (start - 1) * stride : ctr0 + (start - 1);
+      uint32_t up = squares32(cp, key);
+      if (BITREV) up = __brev(up);
+      prev_bit31 = up >> 31;
+    }
+    for (uint64_t i = 0; i < cnt; i++) {
+      const uint64_t z = add64(s.y, key);
+      uint32_t u = squares32_from(s.y, z, s.u);
+      if (BITREV) u = __brev(u);
+      acc += __popc((u ^ (u >> 1)) & 0x7FFFFFFFu);
+      if (start + i > 0) acc += (prev_bit31 ^ u) & 1u;
+      prev_bit31 = u >> 31;
+      if (STRIDED) s.y = add64(s.y, K); else s.y = z;
+      s.u = add64(s.u, s.e);
+      s.e = add64(s.e, k2x2);
+    }
+  }
+  // warp reduction (64-bit), one atomic per warp
+  for (int sh = 16; sh; sh >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sh);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(count, (unsigned long long)acc);
+}
+
+int launch_transitions(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
+                       uint64_t* count, cudaStream_t stream) {
+  const DeviceInfo* di = device_info();
+  if (!di) return SQ_ECUDA;
+  const bool strided = stride != 1, bitrev = (flags & SQ_FUSED_BITREV) != 0;
+  decltype(&transitions_kernel<false, false>) kern =
+      strided ? (bitrev ? transitions_kernel<true, true> : transitions_kernel<true, false>)
+              : (bitrev ? transitions_kernel<false, true> : transitions_kernel<false, false>);
+  uint64_t blocks = (n + 255) / 256;
+  const uint64_t cap = (uint64_t)di->sms * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  const uint64_t T = blocks * 256;
+  kern<<<(unsigned)blocks, 256, 0, stream>>>(key, ctr0, stride, n, n / T, n % T, (unsigned long long*)count);
+  return set_cuda_error(cudaGetLastError());
+}
+
+}  // namespace sq
