@@ -191,6 +191,15 @@ int sq_fused_stats_ex(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, 
 int sq_transitions(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
                    uint64_t* count_dev, sq_stream_t stream);
 
+/* Exhaustive reduced-width uniformity (the desk-scale stand-in for
+ * footnote 1 of P:17, "The probability of any given output is 1/2^32").  For each key k < nkeys
+ * (taken mod 2^W) and EVERY counter c in [0, 2^W), evaluates the W-bit analogue of squares32
+ * (64 -> W and 32 -> W/2 in every square, add, rotation and the final shift) and ACCUMULATES
+ *   hist_dev[k * 2^(W/2) + v] += #{c : squares32_scaled(c, key_k, W) == v}
+ * into caller-zeroed uint64 device memory (nkeys * 2^(W/2) entries).  W even in [8, 32], else
+ * SQ_EINVAL; nkeys <= 65535 per call (else SQ_ERANGE). */
+int sq_scaled_hist(int W, const uint64_t* keys_dev, uint64_t nkeys, uint64_t* hist_dev, sq_stream_t stream);
+
 /* ----------------------------------------------------------------------------------------
  * Host-buffer fill (the end-to-end path): the same map as sq_fill_u32 / sq_fill_u64 /
  * sq_fill_f32 for ONE key, written to HOST memory.  The library generates chunks of

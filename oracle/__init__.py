@@ -75,6 +75,7 @@ def lib() -> ctypes.CDLL:
                 "oracle_keygen": (ctypes.c_int, [u64, u64, P]),
                 "oracle_squares32_scaled": (u64, [u64, u64, ctypes.c_int]),
                 "oracle_gammaq": (ctypes.c_double, [ctypes.c_double, ctypes.c_double]),
+                "oracle_scaled_hist_range": (None, [u64, ctypes.c_int, u64, u64, P]),
                 "oracle_scaled_uniformity": (ctypes.c_int, [u64, ctypes.c_int,
                                                              ctypes.POINTER(ctypes.c_double),
                                                              ctypes.POINTER(ctypes.c_double)]),
@@ -238,6 +239,12 @@ def keygen(seed: int, count: int) -> np.ndarray:
 # ---------------------------------------------------------------- scaled analogue, partition
 def squares32_scaled(ctr: int, key: int, W: int) -> int:
     return lib().oracle_squares32_scaled(ctr & M64, key & M64, W)
+
+
+def scaled_hist_range(key: int, W: int, c0: int, n: int, hist: np.ndarray | None = None) -> np.ndarray:
+    hist = np.zeros(1 << (W // 2), dtype=np.uint64) if hist is None else hist
+    lib().oracle_scaled_hist_range(key & M64, W, c0, n, _ptr(hist))
+    return hist
 
 
 def gammaq(a: float, x: float) -> float:

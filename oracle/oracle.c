@@ -441,6 +441,12 @@ double oracle_gammaq(double a, double x) {
   }
 }
 
+/* Histogram of squares32_scaled over the counters [c0, c0 + n) (a piece of the exhaustive
+ * enumeration; pieces add up).  hist has 2^(W/2) entries. */
+void oracle_scaled_hist_range(uint64_t key, int W, uint64_t c0, uint64_t n, uint64_t* hist) {
+  for (uint64_t c = c0; c < c0 + n; c++) hist[oracle_squares32_scaled(c, key, W)]++;
+}
+
 /* Exhaustive enumeration of all 2^W counters (W even, 8 <= W <= 24), histogram of the
  * 2^(W/2) outputs, chi-square against uniform; p = Q(df/2, chi2/2).  Returns 0 or 1 (bad W). */
 int oracle_scaled_uniformity(uint64_t key, int W, double* chi2_out, double* p_out) {

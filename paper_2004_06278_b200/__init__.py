@@ -73,6 +73,7 @@ def _load() -> ctypes.CDLL:
         "sq_fused_stats": (i32, [u64, u64, u64, vp, vp, vp]),
         "sq_fused_stats_ex": (i32, [u64, u64, u64, u64, u32, vp, vp, vp]),
         "sq_transitions": (i32, [u64, u64, u64, u64, u32, vp, vp]),
+        "sq_scaled_hist": (i32, [i32, vp, u64, vp, vp]),
         "sq_fill_host": (i32, [i32, u64, u64, u64, vp, vp, ctypes.c_size_t, vp, vp]),
     }
     for name, (res, args) in sigs.items():
@@ -86,7 +87,7 @@ def _load() -> ctypes.CDLL:
 EXPORTED_SYMBOLS = ("sq_strerror", "sq_last_cuda_error", "sq_version", "sq_validate_key", "sq_keygen",
                     "sq_fill_u32", "sq_fill_u64", "sq_fill_f32", "sq_fill_u32_k", "sq_fill_u64_k",
                     "sq_fill_f32_k", "sq_fill_f64", "sq_fill_f32x2", "sq_fill_f64_k", "sq_fill_f32x2_k", "sq_fill_ex", "sq_fill_keyctr",
-                    "sq_fused_stats", "sq_fused_stats_ex", "sq_transitions", "sq_fill_host")
+                    "sq_fused_stats", "sq_fused_stats_ex", "sq_transitions", "sq_scaled_hist", "sq_fill_host")
 
 
 def _check(fn: str, code: int) -> None:
@@ -281,6 +282,18 @@ def transitions(key: int, ctr0: int, n: int, stride: int = 1, bitrev: bool = Fal
                                                     SQ_FUSED_BITREV if bitrev else 0, count.data_ptr(),
                                                     _stream_handle(stream)))
     return count
+
+
+def scaled_hist(W: int, keys: torch.Tensor, hist: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Exhaustive W-bit uniformity histograms, shape (nkeys, 2^(W/2)) int64 (accumulating)."""
+    if not (keys.is_cuda and keys.dtype == torch.int64 and keys.dim() == 1 and keys.is_contiguous()):
+        raise ValueError("keys must be a contiguous 1-D int64 CUDA tensor")
+    nb = 1 << (W // 2)
+    if hist is None:
+        hist = torch.zeros((keys.numel(), nb), dtype=torch.int64, device=keys.device)
+    _check("sq_scaled_hist", _load().sq_scaled_hist(int(W), keys.data_ptr(), keys.numel(), hist.data_ptr(),
+                                                    _stream_handle(stream)))
+    return hist
 
 
 def fused_stats(key: int, ctr0: int, n: int, hist: torch.Tensor | None = None,

@@ -110,3 +110,23 @@ def run_battery(key: int, ctr0: int, n: int, stride: int = 1, bitrev: bool = Fal
                 device=None) -> list[TestResult]:
     """The desk battery on n squares32 outputs, computed on the GPU."""
     return statistics(gpu_counts(key, ctr0, n, stride, bitrev, device), alpha)
+
+
+def scaled_uniformity(W: int, keys, device=None) -> list[tuple[float, float]]:
+    """Exhaustive W-bit uniformity (the stand-in for P:17 footnote 1) on the
+    GPU: for each key, every counter 0..2^W-1 of squares32_scaled, chi-square of the 2^(W/2)
+    output counts against uniform; returns [(chi2, p), ...] (df = 2^(W/2) - 1)."""
+    import torch
+
+    from . import scaled_hist
+    k = torch.tensor([int(x) & ((1 << 64) - 1) for x in keys], dtype=torch.uint64).view(torch.int64)
+    k = k.to(device if device is not None else "cuda")
+    out = []
+    for s in range(0, k.numel(), 65535):
+        h = scaled_hist(W, k[s:s + 65535].contiguous())
+        torch.cuda.synchronize(h.device)
+        h = h.cpu().numpy().view(np.uint64).astype(np.float64)
+        e = float(1 << W) / h.shape[1]
+        chi2 = ((h - e) ** 2).sum(axis=1) / e
+        out += [(float(c), _chi2_p(float(c), h.shape[1] - 1)) for c in chi2]
+    return out

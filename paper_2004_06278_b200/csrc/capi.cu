@@ -179,6 +179,14 @@ int sq_transitions(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uin
   return launch_transitions(key, ctr0, stride, n, flags, count_dev, (cudaStream_t)stream);
 }
 
+int sq_scaled_hist(int W, const uint64_t* keys_dev, uint64_t nkeys, uint64_t* hist_dev, sq_stream_t stream) {
+  if (W < 8 || W > 32 || (W & 1)) return SQ_EINVAL;
+  if (nkeys == 0) return SQ_OK;
+  if (!keys_dev || !hist_dev || ((uintptr_t)hist_dev & 7) || ((uintptr_t)keys_dev & 7)) return SQ_EINVAL;
+  if (nkeys > 65535) return SQ_ERANGE;
+  return launch_scaled_hist(W, keys_dev, nkeys, hist_dev, (cudaStream_t)stream);
+}
+
 int sq_fused_stats(uint64_t key, uint64_t ctr0, uint64_t n, uint64_t* hist_dev, uint64_t* ones_dev,
                    sq_stream_t stream) {
   return sq_fused_stats_ex(key, ctr0, 1, n, 0, hist_dev, ones_dev, stream);

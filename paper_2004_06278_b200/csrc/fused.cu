@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "hist16.cuh"
 #include "squares_device.cuh"
 #include "sq_internal.h"
 
@@ -35,45 +36,6 @@ constexpr int kFlushEvery = 63;   // epochs between plane flushes
 constexpr size_t kFusedSmem = 32768 * 4 + 16 * 8 + 16 * 8 + 16 * 4;
 
 static_assert(kFusedThreads * kEpoch <= 0x8000, "epoch bound of the guard-bit scheme");
-
-struct FusedShared {
-  uint32_t* bins;                 // 32768 words
-  unsigned long long* lo_cnt;     // 16: CTA totals for bits 0..15
-  unsigned long long* hi_cnt;     // 16: CTA totals for bits 16..31 from residual bins
-  uint32_t* fix;                  // 16: fix-ups of bins with bit j set
-};
-
-#ifndef SQ_FUSED_INLINE_FIX
-#define SQ_FUSED_INLINE_FIX 0
-#endif
-#ifndef SQ_FUSED_INC_SHIFT
-#define SQ_FUSED_INC_SHIFT 0
-#endif
-#if SQ_FUSED_INLINE_FIX
-__device__ __forceinline__
-#else
-__device__ __noinline__
-#endif
-void guard_fixup(uint32_t* bins, uint32_t b, uint32_t inc,
-                                         unsigned long long* hist, uint32_t* fix) {
-  atomicSub(&bins[b >> 1], inc << 15);                 // half -= 0x8000
-  atomicAdd(&hist[b], 0x8000ull);
-#pragma unroll 1
-  for (int j = 0; j < 16; j++)
-    if ((b >> j) & 1u) atomicAdd(&fix[j], 1u);
-}
-
-__device__ __forceinline__ void hist_add(uint32_t* bins, uint32_t u, unsigned long long* hist,
-                                         uint32_t* fix) {
-  const uint32_t b = u >> 16;
-#if SQ_FUSED_INC_SHIFT
-  const uint32_t inc = 1u << ((u >> 12) & 16u);
-#else
-  const uint32_t inc = (u & 0x10000u) ? 0x10000u : 1u;
-#endif
-  const uint32_t old = atomicAdd(&bins[b >> 1], inc);
-  if (((old + inc) ^ old) & 0x80008000u) guard_fixup(bins, b, inc, hist, fix);
-}
 
 // carry-save adder: (h, l) = (maj(a,b,c), a^b^c)
 __device__ __forceinline__ void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32_t b, uint32_t c) {
@@ -134,11 +96,11 @@ __device__ __forceinline__ void reduce8(const uint32_t (&v)[8], uint32_t (&w)[4]
   for (int i = 0; i < 4; i++) {
     uint32_t a = v[2 * i], b = v[2 * i + 1];
     if (MASKED) {
-      if (base_rem > 2 * i) hist_add(bins, a, hist, fix); else a = 0;
-      if (base_rem > 2 * i + 1) hist_add(bins, b, hist, fix); else b = 0;
+      if (base_rem > 2 * i) hist_add<true>(bins, a, hist, fix); else a = 0;
+      if (base_rem > 2 * i + 1) hist_add<true>(bins, b, hist, fix); else b = 0;
     } else {
-      hist_add(bins, a, hist, fix);
-      hist_add(bins, b, hist, fix);
+      hist_add<true>(bins, a, hist, fix);
+      hist_add<true>(bins, b, hist, fix);
     }
     w[i] = __byte_perm(a, b, 0x5410);
   }

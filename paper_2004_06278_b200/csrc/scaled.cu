@@ -1,0 +1,106 @@
+// scaled.cu -- exhaustive reduced-width uniformity:
+// the W-bit analogue of squares32 (64 -> W and 32 -> W/2 everywhere), evaluated for EVERY
+// counter 0 .. 2^W - 1 of each key, histogrammed over its 2^(W/2) outputs.  This scales the
+// paper's footnote-1 claim ("The probability of any given output is 1/2^32") from the
+// CPU's W <= 24 to W = 32: 2^32 counters per key, a 65536-bin histogram per key.
+//
+// Arithmetic: W <= 32, so every intermediate fits a 32-bit register and x*x mod 2^W is the
+// low W bits of one 32-bit IMAD; the rotation by W/2 is two shifts (a PRMT for W = 32).  The
+// counter walk is the Weyl step y(c+1) = y(c) + key.  The histogram is the packed
+// 16-bit, guard-bit exact scheme of hist16.cuh (epochs of 32 samples per thread).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hist16.cuh"
+#include "sq_internal.h"
+
+namespace sq {
+
+constexpr int kScaledThreads = 1024;
+constexpr int kScaledEpoch = 32;
+static_assert(kScaledThreads * kScaledEpoch <= 0x8000, "guard-bit epoch bound");
+
+struct ScaledArgs {
+  const uint64_t* keys;
+  unsigned long long* hist;   // [nkeys][2^(W/2)]
+  uint64_t slice_len;         // counters per CTA slice (last slice takes the rest)
+  uint32_t W, h, mask;        // width, half width, 2^W - 1
+  uint32_t slices;
+};
+
+__device__ __forceinline__ uint32_t rot_h(uint32_t x, uint32_t h, uint32_t mask) {
+  return ((x >> h) | (x << h)) & mask;
+}
+
+// squares32_scaled for one counter given y = ctr*key and z = y + key (both mod 2^W).
+__device__ __forceinline__ uint32_t scaled_from(uint32_t y, uint32_t z, uint32_t h, uint32_t mask) {
+  uint32_t x = (y * y + y) & mask;        // round 1
+  x = rot_h(x, h, mask);
+  x = (x * x + z) & mask;                 // round 2
+  x = rot_h(x, h, mask);
+  x = (x * x + y) & mask;                 // round 3
+  x = rot_h(x, h, mask);
+  return ((x * x + z) & mask) >> h;       // round 4
+}
+
+__global__ void __launch_bounds__(kScaledThreads, 1) scaled_hist_kernel(ScaledArgs a) {
+  extern __shared__ __align__(16) uint32_t bins[];
+  const uint32_t nbins = 1u << a.h, nwords = (nbins + 1) / 2;
+  for (uint32_t i = threadIdx.x; i < nwords; i += kScaledThreads) bins[i] = 0;
+  __syncthreads();
+  const uint64_t krow = blockIdx.y;
+  const uint32_t key = (uint32_t)(a.keys[krow] & a.mask);
+  const uint64_t total = 1ull << a.W;
+  const uint64_t s0 = (uint64_t)blockIdx.x * a.slice_len;
+  const uint64_t slen = (blockIdx.x == a.slices - 1) ? total - s0 : a.slice_len;
+  const uint64_t q = slen / kScaledThreads, r = slen % kScaledThreads;
+  const uint64_t t = threadIdx.x;
+  const uint64_t start = s0 + t * q + (t < r ? t : r);
+  const uint64_t cnt = q + (t < r ? 1 : 0);
+  const uint64_t epochs = (q + (r ? 1 : 0) + kScaledEpoch - 1) / kScaledEpoch;
+  unsigned long long* hrow = a.hist + krow * nbins;
+  uint32_t y = (uint32_t)(start * key) & a.mask;       // ctr*key mod 2^W
+  uint64_t done = 0;
+  for (uint64_t ep = 0; ep < epochs; ep++) {
+#pragma unroll 4
+    for (int i = 0; i < kScaledEpoch; i++) {
+      const uint32_t z = (y + key) & a.mask;
+      if (done + i < cnt) hist_add<false>(bins, scaled_from(y, z, a.h, a.mask) << 16, hrow, nullptr);
+      y = z;
+    }
+    done += kScaledEpoch;
+    __syncthreads();   // epoch boundary of the guard-bit scheme
+  }
+  for (uint32_t w = threadIdx.x; w < nwords; w += kScaledThreads) {
+    const uint32_t v = bins[w];
+    if (v & 0xFFFFu) atomicAdd(&hrow[2 * w], (unsigned long long)(v & 0xFFFFu));
+    if ((v >> 16) && 2 * w + 1 < nbins) atomicAdd(&hrow[2 * w + 1], (unsigned long long)(v >> 16));
+  }
+}
+
+int launch_scaled_hist(int W, const uint64_t* keys, uint64_t nkeys, uint64_t* hist, cudaStream_t stream) {
+  const DeviceInfo* di = device_info();
+  if (!di) return SQ_ECUDA;
+  if (nkeys > 65535) return SQ_ERANGE;   // grid.y limit; callers batch larger key sets
+  ScaledArgs a;
+  a.keys = keys;
+  a.hist = (unsigned long long*)hist;
+  a.W = (uint32_t)W;
+  a.h = (uint32_t)W / 2;
+  a.mask = (W == 32) ? 0xFFFFFFFFu : ((1u << W) - 1);
+  const uint64_t total = 1ull << W;
+  // slices of >= 2^22 counters, at most one wave of CTAs over all keys
+  uint64_t slices = total >> 22;
+  const uint64_t cap = (uint64_t)di->sms / (nkeys < (uint64_t)di->sms ? nkeys : di->sms);
+  if (slices > cap) slices = cap;
+  if (slices < 1) slices = 1;
+  a.slices = (uint32_t)slices;
+  a.slice_len = total / slices;
+  const size_t smem = (size_t)(((1u << a.h) + 1) / 2) * 4;
+  cudaError_t e = cudaFuncSetAttribute(scaled_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return set_cuda_error(e);
+  scaled_hist_kernel<<<dim3((unsigned)slices, (unsigned)nkeys), kScaledThreads, smem, stream>>>(a);
+  return set_cuda_error(cudaGetLastError());
+}
+
+}  // namespace sq

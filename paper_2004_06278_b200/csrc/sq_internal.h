@@ -54,6 +54,8 @@ int launch_fused(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint3
 int launch_transitions(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
                        uint64_t* count, cudaStream_t stream);
 
+int launch_scaled_hist(int W, const uint64_t* keys, uint64_t nkeys, uint64_t* hist, cudaStream_t stream);
+
 int launch_keyctr(int kind, const uint64_t* keys, uint64_t nkeys, uint64_t ctr, void* out,
                   cudaStream_t stream);
 
