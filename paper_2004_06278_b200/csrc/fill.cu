@@ -102,7 +102,7 @@ __device__ __forceinline__ void gen_lane(const State& s, const RowConst<SPL>& rc
 // KEYIMM: a single row whose key is a kernel parameter, so ptxas can keep the key and the
 // per-row constants in uniform registers (sq_fill_*_k).  Otherwise keys[row] from memory.
 template <int KIND, bool KEYIMM, bool STRIDED>
-__global__ void __launch_bounds__(kFillThreads, kFillMinBlocks) fill_kernel(FillArgs a) {
+__global__ void __launch_bounds__(kFillThreads, KEYIMM ? kFillMinBlocksImm : kFillMinBlocks) fill_kernel(FillArgs a) {
   constexpr int ES = FillTraits<KIND>::ES;
   constexpr int SPL = FillTraits<KIND>::SPL;
   constexpr int LOGJ = FillTraits<KIND>::LOGJ;

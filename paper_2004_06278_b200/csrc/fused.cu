@@ -96,8 +96,11 @@ __device__ __forceinline__ void reduce8(const uint32_t (&v)[8], uint32_t (&w)[4]
   for (int i = 0; i < 4; i++) {
     uint32_t a = v[2 * i], b = v[2 * i + 1];
     if (MASKED) {
-      if (base_rem > 2 * i) hist_add<true>(bins, a, hist, fix); else a = 0;
-      if (base_rem > 2 * i + 1) hist_add<true>(bins, b, hist, fix); else b = 0;
+      const bool va = base_rem > 2 * i, vb = base_rem > 2 * i + 1;
+      hist_add<true>(bins, a, hist, fix, va);
+      hist_add<true>(bins, b, hist, fix, vb);
+      if (!va) a = 0;
+      if (!vb) b = 0;
     } else {
       hist_add<true>(bins, a, hist, fix);
       hist_add<true>(bins, b, hist, fix);

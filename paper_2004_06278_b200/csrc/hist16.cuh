@@ -29,11 +29,14 @@ __device__ __forceinline__ void guard_fixup(uint32_t* bins, uint32_t b, uint32_t
   }
 }
 
-// Count bin (v >> 16) of a 32-bit value v (bin index b < 65536; low half = even bins).
+// Count bin (v >> 16) of a 32-bit value v (bin index b < 65536; low half = even bins).  A lane
+// with valid == false adds 0 (so callers need not diverge around masked samples).
 template <bool BITS>
-__device__ __forceinline__ void hist_add(uint32_t* bins, uint32_t v, unsigned long long* hist, uint32_t* fix) {
+__device__ __forceinline__ void hist_add(uint32_t* bins, uint32_t v, unsigned long long* hist, uint32_t* fix,
+                                         bool valid = true) {
   const uint32_t b = v >> 16;
-  const uint32_t inc = (v & 0x10000u) ? 0x10000u : 1u;
+  uint32_t inc = (v & 0x10000u) ? 0x10000u : 1u;
+  if (!valid) inc = 0;
   const uint32_t old = atomicAdd(&bins[b >> 1], inc);
   if (((old + inc) ^ old) & 0x80008000u) guard_fixup<BITS>(bins, b, inc, hist, fix);
 }

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kScaledThreads, 1) scaled_hist_kernel(ScaledAr
 #pragma unroll 4
     for (int i = 0; i < kScaledEpoch; i++) {
       const uint32_t z = (y + key) & a.mask;
-      if (done + i < cnt) hist_add<false>(bins, scaled_from(y, z, a.h, a.mask) << 16, hrow, nullptr);
+      hist_add<false>(bins, scaled_from(y, z, a.h, a.mask) << 16, hrow, nullptr, done + i < cnt);
       y = z;
     }
     done += kScaledEpoch;

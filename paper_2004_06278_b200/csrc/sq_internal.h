@@ -15,11 +15,17 @@ __host__ __device__ constexpr int kind_elem_bytes(int kind) { return (kind == KI
 #ifndef SQ_FILL_THREADS
 #define SQ_FILL_THREADS 256
 #endif
+// Minimum resident CTAs per SM for the fill kernels (caps registers: 3 -> <= 85, 2 -> <= 128).
+// Measured on B200 (tools/variant_bench.py): 3 for key-by-value, 2 for device keys.
 #ifndef SQ_FILL_MINBLOCKS
-#define SQ_FILL_MINBLOCKS 1
+#define SQ_FILL_MINBLOCKS 2
+#endif
+#ifndef SQ_FILL_MINBLOCKS_IMM
+#define SQ_FILL_MINBLOCKS_IMM 3
 #endif
 constexpr int kFillThreads = SQ_FILL_THREADS;
-constexpr int kFillMinBlocks = SQ_FILL_MINBLOCKS;
+constexpr int kFillMinBlocks = SQ_FILL_MINBLOCKS;         // device-keys kernels
+constexpr int kFillMinBlocksImm = SQ_FILL_MINBLOCKS_IMM;  // key-by-value kernels
 constexpr int kFusedThreads = 1024;
 
 struct FillArgs {
