@@ -102,3 +102,18 @@ def test_fused_ex_matches_fill_bitrev_bincount():
     h1, o1 = O.fused_stats_ex(key, 0, 1, 5000)
     h2, o2 = O.fused_stats(key, 0, 5000)
     assert np.array_equal(h1, h2) and np.array_equal(o1, o2)
+
+
+def test_scaled_hist_range_pieces_and_chi2():
+    """Pieces of the enumeration add up to the whole; the chi-square computed from the whole
+    histogram equals oracle.scaled_uniformity's."""
+    key, W = 0x5A3B, 16
+    whole = O.scaled_hist_range(key, W, 0, 1 << W)
+    parts = np.zeros_like(whole)
+    for c0 in range(0, 1 << W, 1 << 12):
+        O.scaled_hist_range(key, W, c0, 1 << 12, parts)
+    assert np.array_equal(whole, parts) and int(whole.sum()) == 1 << W
+    e = float(1 << W) / whole.size
+    chi2 = float(((whole.astype(np.float64) - e) ** 2).sum() / e)
+    assert abs(chi2 - O.scaled_uniformity(key, W)[0]) < 1e-9
+    assert O.scaled_hist_range(0, W, 0, 1 << W)[0] == 1 << W
