@@ -137,30 +137,42 @@ def oracle_rate(w: SI.Workload, key: int, keys, budget_s: float, threads: int):
         O.fill(kind, [key], 0, m0)
     r1 = m0 / max(time.perf_counter() - t0, 1e-6)
     per = int(max(1 << 16, min(r1 * budget_s, w.samples // threads)))
+    M64 = (1 << 64) - 1
+    lib = O.lib()
+    if w.nkeys > 1:
+        # multi-key workload: each thread fills whole rows (one key each, n counters per row)
+        rows = max(1, per // w.n)
+        per = rows * w.n
+        kk = [np.array([int(keys[(i * rows + r) % len(keys)]) & M64 for r in range(rows)], dtype=np.uint64)
+              for i in range(threads)]
+    else:
+        kk = [np.array([key & M64], dtype=np.uint64) for _ in range(threads)]
+        rows = 1
     bufs = [None] * threads
     if kind != "fused":
         dt = {"u32": np.uint32, "u64": np.uint64, "f32": np.float32}[kind]
         bufs = [np.empty(per, dtype=dt) for _ in range(threads)]
-    lib = O.lib()
     fn = None if kind == "fused" else getattr(lib, f"oracle_fill_{kind}")
-    karr = [np.array([int(keys[i % len(keys)]) if w.nkeys > 1 else key], dtype=np.uint64) for i in range(threads)]
 
     def work(i):
-        start = (w.samples // threads) * i if w.nkeys == 1 else 0
         if kind == "fused":
             h = np.zeros(65536, np.uint64)
             o = np.zeros(32, np.uint64)
-            lib.oracle_fused_stats(key, start, per, h.ctypes.data, o.ctypes.data)
+            lib.oracle_fused_stats(key & M64, (w.samples // threads) * i, per, h.ctypes.data, o.ctypes.data)
+        elif w.nkeys > 1:
+            fn(kk[i].ctypes.data, rows, w.ctr0, w.n, bufs[i].ctypes.data, w.n)
         else:
-            fn(karr[i].ctypes.data, 1, start, per, bufs[i].ctypes.data, per)
+            fn(kk[i].ctypes.data, 1, (w.samples // threads) * i, per, bufs[i].ctypes.data, per)
 
     with ThreadPoolExecutor(threads) as ex:
         t0 = time.perf_counter()
         list(ex.map(work, range(threads)))
         wall = time.perf_counter() - t0
     total = per * threads
-    shape = (f"{threads} threads x {per} consecutive counters" +
-             (" (one key row each)" if w.nkeys > 1 else " (disjoint shards of the workload's counter range)"))
+    if w.nkeys > 1:
+        shape = f"{threads} threads x {rows} key rows x {w.n} counters (the workload's row shape)"
+    else:
+        shape = f"{threads} threads x {per} consecutive counters (disjoint shards of the workload's counter range)"
     return total / wall, total, wall, shape
 
 

@@ -28,6 +28,10 @@ __device__ __forceinline__ void rr(uint32_t& xh, uint32_t& xl, uint64_t w, uint3
   if (DBL == 0) hi = (uint32_t)(t >> 32) + xl * (xh << 1);
   else if (DBL == 1) hi = (uint32_t)(t >> 32) + xl * shl1(xh);
   else if (DBL == 2) { uint32_t c = xl * xh; hi = (uint32_t)(t >> 32) + (c << 1); }
+  else if (DBL == 5) {   // c = xl*xh (2-operand IMAD), hi = hi(t) + c + c (3-input IADD3 doubles for free)
+    uint32_t c; asm("mul.lo.u32 %0, %1, %2;" : "=r"(c) : "r"(xl), "r"(xh));
+    asm("add.u32 %0, %1, %2;\n\tadd.u32 %0, %0, %2;" : "=r"(hi) : "r"((uint32_t)(t >> 32)), "r"(c));
+  }
   else hi = (uint32_t)(t >> 32) + xl * dbl<DBL>(xh, zr);
   xh = (uint32_t)t; xl = hi;
 }
@@ -37,6 +41,11 @@ __device__ __forceinline__ uint32_t rh(uint32_t xh, uint32_t xl, uint64_t w, uin
   if (DBL == 0) return (uint32_t)(t >> 32) + xl * (xh << 1);
   if (DBL == 1) return (uint32_t)(t >> 32) + xl * shl1(xh);
   if (DBL == 2) { uint32_t c = xl * xh; return (uint32_t)(t >> 32) + (c << 1); }
+  if (DBL == 5) {
+    uint32_t c, h; asm("mul.lo.u32 %0, %1, %2;" : "=r"(c) : "r"(xl), "r"(xh));
+    asm("add.u32 %0, %1, %2;\n\tadd.u32 %0, %0, %2;" : "=r"(h) : "r"((uint32_t)(t >> 32)), "r"(c));
+    return h;
+  }
   return (uint32_t)(t >> 32) + xl * dbl<DBL>(xh, zr);
 }
 
@@ -102,6 +111,9 @@ static int run(K kern, const char* name, int spl) {
 }
 
 int main() {
+  run(kloop<0, 5, 16>, "F0_D5_S16", 16);
+  run(kloop<0, 5, 8>, "F0_D5_S8", 8);
+  run(kloop<2, 5, 8>, "F2_D5_S8", 8);
   run(kloop<0, 3, 16>, "F0_D3_S16", 16);
   run(kloop<0, 4, 16>, "F0_D4_S16", 16);
   run(kloop<0, 3, 8>, "F0_D3_S8", 8);
