@@ -381,9 +381,16 @@ def main():
 
     import torch
     import torch.distributed as tdist
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink/NVSwitch; SQ_BENCH_BACKEND=gloo only to exercise the multi-rank logic
+        # with several ranks on one GPU (no collective on the fill data path either way)
+        backend = os.environ.get("SQ_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group(backend)
     peaks, peaks_src = load_peaks()
     prof = load_profile_summary()
     import paper_2004_06278_b200 as sq  # noqa: F401  (loads libsquares.so; raises if missing)

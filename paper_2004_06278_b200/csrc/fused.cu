@@ -30,9 +30,13 @@
 
 namespace sq {
 
-constexpr int kEpoch = 32;        // samples per thread per epoch (x1024 threads = 0x8000)
-constexpr int kPlanes = 6;        // vertical planes for weight-16 words: counts up to 63
-constexpr int kFlushEvery = 63;   // epochs between plane flushes
+constexpr int kEpoch = 0x8000 / kFusedThreads;   // samples per thread per epoch (x threads = 0x8000)
+constexpr int kTrees = kEpoch / 32;               // 16-word Harley-Seal trees per epoch
+constexpr int kPlanes = 6;                        // vertical planes for weight-16 words: counts up to 63
+constexpr int kFlushEvery = 63 / kTrees;          // epochs between plane flushes
+constexpr int kWordsPerThread = 32768 / kFusedThreads;
+constexpr int kLogW = (kWordsPerThread == 32) ? 5 : 6;
+static_assert(kEpoch % 32 == 0 && (1 << kLogW) == kWordsPerThread, "fused geometry");
 constexpr size_t kFusedSmem = 32768 * 4 + 16 * 8 + 16 * 8 + 16 * 4;
 
 static_assert(kFusedThreads * kEpoch <= 0x8000, "epoch bound of the guard-bit scheme");
@@ -176,21 +180,24 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
   uint64_t done = 0;
   int since_flush = 0;
   for (uint32_t ep = 0; ep < epochs; ep++) {
-    uint32_t sixteens;
-    if (done + kEpoch <= cnt) {
-      sixteens = epoch<false, STRIDED, BITREV>(s, wc, bins, hist, fix, kEpoch, ones, twos, fours, eights);
-    } else {
-      const int64_t rem = done < cnt ? (int64_t)(cnt - done) : 0;
-      sixteens = epoch<true, STRIDED, BITREV>(s, wc, bins, hist, fix, rem, ones, twos, fours, eights);
-    }
-    done += kEpoch;
-    // ripple-add the weight-16 word into the vertical planes
-    uint32_t c = sixteens;
 #pragma unroll
-    for (int p = 0; p < kPlanes; p++) {
-      const uint32_t tt = pl[p] & c;
-      pl[p] ^= c;
-      c = tt;
+    for (int tr = 0; tr < kTrees; tr++) {
+      uint32_t sixteens;
+      if (done + 32 <= cnt) {
+        sixteens = epoch<false, STRIDED, BITREV>(s, wc, bins, hist, fix, 32, ones, twos, fours, eights);
+      } else {
+        const int64_t rem = done < cnt ? (int64_t)(cnt - done) : 0;
+        sixteens = epoch<true, STRIDED, BITREV>(s, wc, bins, hist, fix, rem, ones, twos, fours, eights);
+      }
+      done += 32;
+      // ripple-add the weight-16 word into the vertical planes
+      uint32_t c = sixteens;
+#pragma unroll
+      for (int p = 0; p < kPlanes; p++) {
+        const uint32_t tt = pl[p] & c;
+        pl[p] ^= c;
+        c = tt;
+      }
     }
     if (++since_flush == kFlushEvery) {   // planes hold <= 63 per column: flush to the CTA totals
       since_flush = 0;
@@ -210,25 +217,29 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
   warp_flush16(colcnt, lo_cnt);
 
   // residual bins -> global hist; bits 16..31 derived from the residual bins.
-  // Thread tid owns words [32*tid, 32*tid+32) = bins [64*tid, 64*tid+64): bins' bits 6..15
-  // are tid's bits; the word index i (rotated by lane for conflict-free banks) gives bits 1..5.
-  uint32_t T = 0, S[6] = {0, 0, 0, 0, 0, 0};
+  // Thread tid owns words [W*tid, W*tid+W) (W = kWordsPerThread) = bins [2W*tid, 2W*tid+2W):
+  // a bin's bit 0 is the half, bits 1..kLogW the word index i (rotated by lane for
+  // conflict-free banks), and the higher bits are tid's bits.
+  uint32_t T = 0, S[kLogW + 1];
+#pragma unroll
+  for (int j = 0; j <= kLogW; j++) S[j] = 0;
   const uint32_t lane = tid & 31;
 #pragma unroll 4
-  for (uint32_t k = 0; k < 32; k++) {
-    const uint32_t i = (k + lane) & 31;
-    const uint32_t wv = bins[32 * tid + i];
+  for (uint32_t k = 0; k < kWordsPerThread; k++) {
+    const uint32_t i = (k + lane) & (kWordsPerThread - 1);
+    const uint32_t wv = bins[kWordsPerThread * tid + i];
     const uint32_t lo = wv & 0xFFFFu, hi = wv >> 16;
-    const uint32_t b0 = 64 * tid + 2 * i;
+    const uint32_t b0 = 2 * kWordsPerThread * tid + 2 * i;
     if (lo) atomicAdd(&hist[b0], (unsigned long long)lo);
     if (hi) atomicAdd(&hist[b0 + 1], (unsigned long long)hi);
     T += lo + hi;
     S[0] += hi;
 #pragma unroll
-    for (int j = 1; j < 6; j++) S[j] += ((i >> (j - 1)) & 1u) ? (lo + hi) : 0u;
+    for (int j = 1; j <= kLogW; j++) S[j] += ((i >> (j - 1)) & 1u) ? (lo + hi) : 0u;
   }
 #pragma unroll
-  for (int j = 0; j < 16; j++) colcnt[j] = (j < 6) ? S[j] : (((tid >> (j - 6)) & 1u) ? T : 0u);
+  for (int j = 0; j < 16; j++)
+    colcnt[j] = (j <= kLogW) ? S[j] : (((tid >> (j - 1 - kLogW)) & 1u) ? T : 0u);
   warp_flush16(colcnt, hi_cnt);
   __syncthreads();
   if (tid < 16) {

@@ -26,7 +26,10 @@ __host__ __device__ constexpr int kind_elem_bytes(int kind) { return (kind == KI
 constexpr int kFillThreads = SQ_FILL_THREADS;
 constexpr int kFillMinBlocks = SQ_FILL_MINBLOCKS;         // device-keys kernels
 constexpr int kFillMinBlocksImm = SQ_FILL_MINBLOCKS_IMM;  // key-by-value kernels
-constexpr int kFusedThreads = 1024;
+#ifndef SQ_FUSED_THREADS
+#define SQ_FUSED_THREADS 1024
+#endif
+constexpr int kFusedThreads = SQ_FUSED_THREADS;   // 1024 (epochs of 32 samples) or 512 (64)
 
 struct FillArgs {
   const uint64_t* keys;     // device keys, or nullptr to use key_imm (single row)
