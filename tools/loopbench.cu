@@ -38,6 +38,10 @@ __device__ __forceinline__ void rr(uint32_t& xh, uint32_t& xl, uint64_t w, uint3
 template <int DBL>
 __device__ __forceinline__ uint32_t rh(uint32_t xh, uint32_t xl, uint64_t w, uint32_t zr) {
   uint64_t t = (uint64_t)xl * xl + w;
+  if (DBL == 6) {   // keep the low word alive so ptxas emits IMAD.WIDE instead of IMAD.HI
+    asm volatile("" :: "r"((uint32_t)t));
+    return (uint32_t)(t >> 32) + xl * (xh << 1);
+  }
   if (DBL == 0) return (uint32_t)(t >> 32) + xl * (xh << 1);
   if (DBL == 1) return (uint32_t)(t >> 32) + xl * shl1(xh);
   if (DBL == 2) { uint32_t c = xl * xh; return (uint32_t)(t >> 32) + (c << 1); }
@@ -111,6 +115,9 @@ static int run(K kern, const char* name, int spl) {
 }
 
 int main() {
+  run(kloop<0, 6, 16>, "F0_D6_S16", 16);
+  run(kloop<0, 0, 16>, "F0_D0_S16", 16);
+  run(kloop<0, 6, 8>, "F0_D6_S8", 8);
   run(kloop<0, 5, 16>, "F0_D5_S16", 16);
   run(kloop<0, 5, 8>, "F0_D5_S8", 8);
   run(kloop<2, 5, 8>, "F2_D5_S8", 8);
