@@ -65,38 +65,68 @@ __device__ __forceinline__ uint64_t add64_3(uint64_t a, uint64_t b, uint64_t c) 
   return d;
 }
 
+// hi + lo32(2 * xl * xh): the cross term of a square.  `one` is the value 1 held in a register
+// the compiler cannot see through (a kernel argument); FORM selects the instruction shape:
+//   0  IMAD(xl, xh << 1, hi)                 -- the shortest form; ptxas may place the doubling
+//                                               on the IMAD pipe
+//   1  IMAD(xl, xh << one, hi)               -- the doubling is a variable shift: ALU only
+//   2  hi + ((xl * xh) << one)               -- IMAD without addend runs beside the round's
+//                                               IMAD.WIDE; only an IADD3 follows the WIDE on the
+//                                               dependency chain (shorter latency per round)
+#ifndef SQ_ROUND_FORM
+#define SQ_ROUND_FORM 0
+#endif
+template <int FORM = SQ_ROUND_FORM>
+__device__ __forceinline__ uint32_t cross_add(uint32_t xl, uint32_t xh, uint32_t hi, uint32_t one) {
+  if (FORM == 0) return mad_lo(xl, xh << 1, hi);
+  uint32_t d;
+  if (FORM == 1) {
+    asm("shl.b32 %0, %1, %2;" : "=r"(d) : "r"(xh), "r"(one));
+    return mad_lo(xl, d, hi);
+  }
+  uint32_t c;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(c) : "r"(xl), "r"(xh));
+  asm("shl.b32 %0, %1, %2;" : "=r"(d) : "r"(c), "r"(one));
+  asm("add.u32 %0, %1, %2;" : "=r"(c) : "r"(hi), "r"(d));
+  return c;
+}
+
 // x <- rot32(x*x + w), x held as (xh, xl).  P:24-26.
-__device__ __forceinline__ void round_rot(uint32_t& xh, uint32_t& xl, uint64_t w) {
+template <int FORM = SQ_ROUND_FORM>
+__device__ __forceinline__ void round_rot(uint32_t& xh, uint32_t& xl, uint64_t w, uint32_t one = 1) {
   uint64_t t = mad_wide(xl, xl, w);
-  uint32_t hi = mad_lo(xl, xh << 1, hi32(t));
+  uint32_t hi = cross_add<FORM>(xl, xh, hi32(t), one);
   xh = lo32(t);
   xl = hi;
 }
 
 // High 32 bits of x*x + w (the final extraction of P:27 and P:63).
-__device__ __forceinline__ uint32_t round_hi(uint32_t xh, uint32_t xl, uint64_t w) {
+template <int FORM = SQ_ROUND_FORM>
+__device__ __forceinline__ uint32_t round_hi(uint32_t xh, uint32_t xl, uint64_t w, uint32_t one = 1) {
   uint64_t t = mad_wide(xl, xl, w);
-  return mad_lo(xl, xh << 1, hi32(t));
+  return cross_add<FORM>(xl, xh, hi32(t), one);
 }
 
 // squares32 given y = ctr*key, z = y + key and u = y*y + y (round 1's sum).  P:21-28.
-__device__ __forceinline__ uint32_t squares32_from(uint64_t y, uint64_t z, uint64_t u) {
+template <int FORM = SQ_ROUND_FORM>
+__device__ __forceinline__ uint32_t squares32_from(uint64_t y, uint64_t z, uint64_t u, uint32_t one = 1) {
   uint32_t xh = lo32(u), xl = hi32(u);  // round 1: rot32(u)
-  round_rot(xh, xl, z);             // round 2
-  round_rot(xh, xl, y);             // round 3
-  return round_hi(xh, xl, z);       // round 4
+  round_rot<FORM>(xh, xl, z, one);      // round 2
+  round_rot<FORM>(xh, xl, y, one);      // round 3
+  return round_hi<FORM>(xh, xl, z, one);  // round 4
 }
 
 // squares64 given y, z, u as above.  P:56-64: t = x*x + z (round 4, kept before rotating),
 // result t ^ ((rot32(t)^2 + y) >> 32); only t's low half changes.
-__device__ __forceinline__ uint64_t squares64_from(uint64_t y, uint64_t z, uint64_t u) {
+template <int FORM = SQ_ROUND_FORM>
+__device__ __forceinline__ uint64_t squares64_from(uint64_t y, uint64_t z, uint64_t u, uint32_t one = 1) {
   uint32_t xh = lo32(u), xl = hi32(u);
-  round_rot(xh, xl, z);             // round 2
-  round_rot(xh, xl, y);             // round 3
+  round_rot<FORM>(xh, xl, z, one);      // round 2
+  round_rot<FORM>(xh, xl, y, one);      // round 3
   uint64_t t = mad_wide(xl, xl, z);     // round 4 (full 64-bit sum)
-  uint32_t th = mad_lo(xl, xh << 1, hi32(t));
+  uint32_t th = cross_add<FORM>(xl, xh, hi32(t), one);
   uint32_t tl = lo32(t);
-  uint32_t r5 = round_hi(tl, th, y);  // round 5 on rot32(t) = (tl, th)
+  uint32_t r5 = round_hi<FORM>(tl, th, y, one);  // round 5 on rot32(t) = (tl, th)
   return ((uint64_t)th << 32) | (uint64_t)(tl ^ r5);
 }
 

@@ -65,6 +65,7 @@ static int fill_any(int kind, const uint64_t* keys_dev, uint64_t nkeys, uint64_t
   a.key_imm = key_imm;
   a.ctr0 = ctr0;
   a.stride = stride;
+  a.one = 1;
   a.n = n;
   a.out = (char*)out_dev;
   a.ld_bytes = ld * es;
@@ -225,6 +226,7 @@ int sq_fill_host(int kind, uint64_t key, uint64_t ctr0, uint64_t n, void* out_ho
     a.key_imm = key;
     a.ctr0 = ctr0 + done;
     a.stride = 1;
+    a.one = 1;
     a.n = m;
     a.out = buf;
     a.ld_bytes = m * es;

@@ -62,12 +62,12 @@ __device__ __forceinline__ RowConst<SPL> row_const(uint64_t key, uint64_t stride
 
 // Output words of one sample j of kind KIND into v (little-endian 64-bit elements).
 template <int KIND>
-__device__ __forceinline__ void put(uint32_t (&v)[16], int j, uint64_t y, uint64_t z, uint64_t u) {
+__device__ __forceinline__ void put(uint32_t (&v)[16], int j, uint64_t y, uint64_t z, uint64_t u, uint32_t one) {
   if (KIND == KIND_U32 || KIND == KIND_F32) {
-    const uint32_t o = squares32_from(y, z, u);
+    const uint32_t o = squares32_from(y, z, u, one);
     v[j] = (KIND == KIND_F32) ? __float_as_uint(u32_to_unit_f32(o)) : o;
   } else {
-    const uint64_t o = squares64_from(y, z, u);
+    const uint64_t o = squares64_from(y, z, u, one);
     if (KIND == KIND_U64) {
       v[2 * j] = lo32(o);
       v[2 * j + 1] = hi32(o);
@@ -86,12 +86,12 @@ __device__ __forceinline__ void put(uint32_t (&v)[16], int j, uint64_t y, uint64
 // (STRIDED = false): z = y + key is the next counter's y.  Strided: y steps by K and
 // z = y + key separately (one more 64-bit add per sample).
 template <int KIND, int SPL, bool STRIDED>
-__device__ __forceinline__ void gen_lane(const State& s, const RowConst<SPL>& rc, uint32_t (&v)[16]) {
+__device__ __forceinline__ void gen_lane(const State& s, const RowConst<SPL>& rc, uint32_t (&v)[16], uint32_t one) {
   uint64_t y = s.y, u = s.u;
 #pragma unroll
   for (int j = 0; j < SPL; j++) {
     const uint64_t z = add64(y, rc.key);
-    put<KIND>(v, j, y, z, u);
+    put<KIND>(v, j, y, z, u, one);
     if (j < SPL - 1) {
       y = STRIDED ? add64(y, rc.K) : z;
       u = j ? add64_3(u, s.e, rc.cst[j]) : add64(u, s.e);
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kFillThreads, KEYIMM ? kFillMinBlocksImm : kFi
         i0 += nfull * J;
         cc += nfull;
         for (; nfull; nfull--) {
-          gen_lane<KIND, SPL, STRIDED>(s, rc, v);
+          gen_lane<KIND, SPL, STRIDED>(s, rc, v, a.one);
 #ifdef SQ_FILL_NOSTORE   // experiment: generation without the output stream
 #pragma unroll
           for (int j = 0; j < 16; j++) nostore_acc ^= v[j];
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kFillThreads, KEYIMM ? kFillMinBlocksImm : kFi
         }
       } else {
         // boundary chunk (row head or ragged tail): per-element masked stores
-        gen_lane<KIND, SPL, STRIDED>(s, rc, v);
+        gen_lane<KIND, SPL, STRIDED>(s, rc, v, a.one);
         char* p = rowp + (int64_t)i0 * ES;
 #pragma unroll
         for (int j = 0; j < SPL; j++) {

@@ -76,12 +76,13 @@ struct WalkConst {
 // STRIDED: counters advance by `stride` (y by K, z = y + key separately); BITREV: each
 // output is bit-reversed before it is counted ("bits-reversed tests").
 template <bool STRIDED, bool BITREV>
-__device__ __forceinline__ void gen8(State& s, const WalkConst& wc, uint32_t (&v)[8]) {
+__device__ __forceinline__ void gen8(State& s, const WalkConst& wc, uint32_t (&v)[8], uint32_t one) {
   uint64_t y = s.y, u = s.u;
 #pragma unroll
   for (int j = 0; j < 8; j++) {
     const uint64_t z = add64(y, wc.key);
-    const uint32_t o = squares32_from(y, z, u);
+    // FORM 1 (doubling as a variable shift, ALU pipe): +3.5 % here on B200
+    const uint32_t o = squares32_from<1>(y, z, u, one);
     v[j] = BITREV ? __brev(o) : o;
     y = STRIDED ? add64(y, wc.K) : z;
     u = j ? add64_3(u, s.e, wc.cst[j]) : add64(u, s.e);
@@ -115,7 +116,7 @@ __device__ __forceinline__ void reduce8(const uint32_t (&v)[8], uint32_t (&w)[4]
 
 // One epoch (32 samples = 16 packed words) folded by Harley-Seal into a weight-16 word.
 template <bool MASKED, bool STRIDED, bool BITREV>
-__device__ __forceinline__ uint32_t epoch(State& s, const WalkConst& wc, uint32_t* bins,
+__device__ __forceinline__ uint32_t epoch(State& s, const WalkConst& wc, uint32_t one, uint32_t* bins,
                                           unsigned long long* hist, uint32_t* fix, int64_t rem,
                                           uint32_t& ones, uint32_t& twos, uint32_t& fours,
                                           uint32_t& eights) {
@@ -126,7 +127,7 @@ __device__ __forceinline__ uint32_t epoch(State& s, const WalkConst& wc, uint32_
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       uint32_t v[8], w[4], twosA, twosB;
-      gen8<STRIDED, BITREV>(s, wc, v);
+      gen8<STRIDED, BITREV>(s, wc, v, one);
       reduce8<MASKED>(v, w, bins, hist, fix, rem - 8 * (2 * blk + h));
       csa(twosA, ones, ones, w[0], w[1]);
       csa(twosB, ones, ones, w[2], w[3]);
@@ -142,7 +143,7 @@ __device__ __forceinline__ uint32_t epoch(State& s, const WalkConst& wc, uint32_
 template <bool STRIDED, bool BITREV>
 __global__ void __launch_bounds__(kFusedThreads, 1)
 fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t r, uint32_t epochs,
-             unsigned long long* __restrict__ hist, unsigned long long* __restrict__ ones_out) {
+             unsigned long long* __restrict__ hist, unsigned long long* __restrict__ ones_out, uint32_t one) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* bins = smem;
   unsigned long long* lo_cnt = (unsigned long long*)(smem + 32768);
@@ -184,10 +185,10 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
     for (int tr = 0; tr < kTrees; tr++) {
       uint32_t sixteens;
       if (done + 32 <= cnt) {
-        sixteens = epoch<false, STRIDED, BITREV>(s, wc, bins, hist, fix, 32, ones, twos, fours, eights);
+        sixteens = epoch<false, STRIDED, BITREV>(s, wc, one, bins, hist, fix, 32, ones, twos, fours, eights);
       } else {
         const int64_t rem = done < cnt ? (int64_t)(cnt - done) : 0;
-        sixteens = epoch<true, STRIDED, BITREV>(s, wc, bins, hist, fix, rem, ones, twos, fours, eights);
+        sixteens = epoch<true, STRIDED, BITREV>(s, wc, one, bins, hist, fix, rem, ones, twos, fours, eights);
       }
       done += 32;
       // ripple-add the weight-16 word into the vertical planes
@@ -270,7 +271,7 @@ int launch_fused(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint3
   const uint64_t epochs = (per + kEpoch - 1) / kEpoch;
   if (epochs > 0xFFFFFFFFull) return SQ_ERANGE;
   kern<<<(unsigned)blocks, kFusedThreads, kFusedSmem, stream>>>(
-      key, ctr0, stride, q, r, (uint32_t)epochs, (unsigned long long*)hist, (unsigned long long*)ones);
+      key, ctr0, stride, q, r, (uint32_t)epochs, (unsigned long long*)hist, (unsigned long long*)ones, 1u);
   return set_cuda_error(cudaGetLastError());
 }
 

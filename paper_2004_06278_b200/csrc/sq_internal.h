@@ -41,6 +41,7 @@ struct FillArgs {
   uint64_t ld_bytes;        // row pitch in bytes
   uint64_t chunks_per_row;  // set by the launcher
   uint64_t chunks_q, chunks_r;  // balanced split of all chunks over the grid's warps
+  uint32_t one;             // always 1: the opaque shift amount of squares_dev.cuh cross_add
 };
 
 struct DeviceInfo {

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s line %d\n", cudaGetErrorString(e_), __LINE__); return 1; } } while (0)
 
@@ -17,6 +18,7 @@ __device__ uint32_t g_zr;   // unused; zr comes from a kernel parameter
 template <int DBL>
 __device__ __forceinline__ uint32_t dbl(uint32_t x, uint32_t zr) {
   uint32_t d;
+  if (DBL == 7) { asm("shl.b32 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(zr)); return d; }   // zr = 1: opaque shift
   if (DBL == 3) asm("add.u32 %0, %1, %1;\n\tadd.u32 %0, %0, %2;" : "=r"(d) : "r"(x), "r"(zr));
   else asm("shf.l.clamp.b32 %0, %2, %1, 1;" : "=r"(d) : "r"(x), "r"(zr));
   return d;
@@ -97,13 +99,14 @@ static int run(K kern, const char* name, int spl) {
   int iters = 4096 / spl * 8;
   uint32_t* out; CK(cudaMalloc(&out, 4));
   cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, kern);
-  kern<<<blocks, 256>>>(0x1fac726d8cb5432full, 0, iters, out, 0u);
+  const uint32_t zr = strstr(name, "_D7_") ? 1u : 0u;
+  kern<<<blocks, 256>>>(0x1fac726d8cb5432full, 0, iters, out, zr);
   CK(cudaDeviceSynchronize());
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   float best = 1e9;
   for (int r = 0; r < 5; r++) {
     cudaEventRecord(a);
-    kern<<<blocks, 256>>>(0x1fac726d8cb5432full, 0, iters, out, 0u);
+    kern<<<blocks, 256>>>(0x1fac726d8cb5432full, 0, iters, out, zr);
     cudaEventRecord(b);
     CK(cudaEventSynchronize(b));
     float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
@@ -115,6 +118,8 @@ static int run(K kern, const char* name, int spl) {
 }
 
 int main() {
+  run(kloop<0, 7, 16>, "F0_D7_S16", 16);
+  run(kloop<0, 7, 8>, "F0_D7_S8", 8);
   run(kloop<0, 6, 16>, "F0_D6_S16", 16);
   run(kloop<0, 0, 16>, "F0_D0_S16", 16);
   run(kloop<0, 6, 8>, "F0_D6_S8", 8);
