@@ -205,11 +205,20 @@ int sq_fill_host(int kind, uint64_t key, uint64_t ctr0, uint64_t n, void* out_ho
   if (chunk == 0) return SQ_EINVAL;
   cudaStream_t gs = (cudaStream_t)stream, cs = (cudaStream_t)copy_stream;
   if (cs == gs) cs = nullptr;
-  cudaEvent_t gen_done[2], copy_done[2];
+  cudaEvent_t gen_done[2] = {nullptr, nullptr}, copy_done[2] = {nullptr, nullptr};
+  auto destroy_events = [&]() {
+    for (int i = 0; i < 2; i++) {
+      if (gen_done[i]) cudaEventDestroy(gen_done[i]);
+      if (copy_done[i]) cudaEventDestroy(copy_done[i]);
+    }
+  };
   for (int b = 0; b < 2; b++) {
     cudaError_t e = cudaEventCreateWithFlags(&gen_done[b], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copy_done[b], cudaEventDisableTiming);
-    if (e != cudaSuccess) return set_cuda_error(e);
+    if (e != cudaSuccess) {
+      destroy_events();
+      return set_cuda_error(e);
+    }
   }
   int rc = SQ_OK;
   uint64_t done = 0;
@@ -245,7 +254,7 @@ int sq_fill_host(int kind, uint64_t key, uint64_t ctr0, uint64_t n, void* out_ho
   }
   cudaError_t e1 = cudaStreamSynchronize(gs);
   cudaError_t e2 = cs ? cudaStreamSynchronize(cs) : cudaSuccess;
-  for (int i = 0; i < 2; i++) { cudaEventDestroy(gen_done[i]); cudaEventDestroy(copy_done[i]); }
+  destroy_events();
   if (rc != SQ_OK) return rc;
   if (e1 != cudaSuccess) return set_cuda_error(e1);
   return set_cuda_error(e2);

@@ -61,13 +61,16 @@ __device__ __forceinline__ RowConst<SPL> row_const(uint64_t key, uint64_t stride
 }
 
 // Output words of one sample j of kind KIND into v (little-endian 64-bit elements).
-template <int KIND>
+#ifndef SQ_FILL_FORM
+#define SQ_FILL_FORM 0
+#endif
+template <int KIND, int FORM>
 __device__ __forceinline__ void put(uint32_t (&v)[16], int j, uint64_t y, uint64_t z, uint64_t u, uint32_t one) {
   if (KIND == KIND_U32 || KIND == KIND_F32) {
-    const uint32_t o = squares32_from(y, z, u, one);
+    const uint32_t o = squares32_from<FORM>(y, z, u, one);
     v[j] = (KIND == KIND_F32) ? __float_as_uint(u32_to_unit_f32(o)) : o;
   } else {
-    const uint64_t o = squares64_from(y, z, u, one);
+    const uint64_t o = squares64_from<FORM>(y, z, u, one);
     if (KIND == KIND_U64) {
       v[2 * j] = lo32(o);
       v[2 * j + 1] = hi32(o);
@@ -85,13 +88,25 @@ __device__ __forceinline__ void put(uint32_t (&v)[16], int j, uint64_t y, uint64
 // The SPL outputs of one lane from state s (not modified).  Consecutive counters
 // (STRIDED = false): z = y + key is the next counter's y.  Strided: y steps by K and
 // z = y + key separately (one more 64-bit add per sample).
+#ifndef SQ_FILL_Y3
+#define SQ_FILL_Y3 0
+#endif
 template <int KIND, int SPL, bool STRIDED>
 __device__ __forceinline__ void gen_lane(const State& s, const RowConst<SPL>& rc, uint32_t (&v)[16], uint32_t one) {
   uint64_t y = s.y, u = s.u;
+#if SQ_FILL_Y3
+  // y + key as a 3-input add y + (key - one) + one with the opaque one: IMAD cannot express a
+  // 3-input add, so both halves stay on the ALU pipe (IADD3 / IADD3.X with two carries)
+  const uint64_t km1 = rc.key - one, one64 = one;
+#endif
 #pragma unroll
   for (int j = 0; j < SPL; j++) {
+#if SQ_FILL_Y3
+    const uint64_t z = add64_3(y, km1, one64);
+#else
     const uint64_t z = add64(y, rc.key);
-    put<KIND>(v, j, y, z, u, one);
+#endif
+    put<KIND, SQ_FILL_FORM>(v, j, y, z, u, one);
     if (j < SPL - 1) {
       y = STRIDED ? add64(y, rc.K) : z;
       u = j ? add64_3(u, s.e, rc.cst[j]) : add64(u, s.e);
