@@ -73,6 +73,8 @@ __device__ __forceinline__ uint64_t add64_3(uint64_t a, uint64_t b, uint64_t c) 
 //   2  hi + ((xl * xh) << one)               -- IMAD without addend runs beside the round's
 //                                               IMAD.WIDE; only an IADD3 follows the WIDE on the
 //                                               dependency chain (shorter latency per round)
+//   3  IMAD(xl, SHF(RZ:xh, 1), hi)           -- the doubling as a funnel shift with an immediate
+//                                               amount: ALU pipe, one register read
 #ifndef SQ_ROUND_FORM
 #define SQ_ROUND_FORM 0
 #endif
@@ -80,6 +82,10 @@ template <int FORM = SQ_ROUND_FORM>
 __device__ __forceinline__ uint32_t cross_add(uint32_t xl, uint32_t xh, uint32_t hi, uint32_t one) {
   if (FORM == 0) return mad_lo(xl, xh << 1, hi);
   uint32_t d;
+  if (FORM == 3) {
+    asm("shf.l.clamp.b32 %0, 0, %1, 1;" : "=r"(d) : "r"(xh));
+    return mad_lo(xl, d, hi);
+  }
   if (FORM == 1) {
     asm("shl.b32 %0, %1, %2;" : "=r"(d) : "r"(xh), "r"(one));
     return mad_lo(xl, d, hi);

@@ -61,9 +61,13 @@ __device__ __forceinline__ RowConst<SPL> row_const(uint64_t key, uint64_t stride
 }
 
 // Output words of one sample j of kind KIND into v (little-endian 64-bit elements).
+// Cross-term form (squares_dev.cuh cross_add) per output kind, measured on B200
+// (DESIGN.md 7.5): the funnel-shift doubling (3) for the u32 fill, the plain form (0) else.
 #ifndef SQ_FILL_FORM
-#define SQ_FILL_FORM 0
+#define SQ_FILL_FORM -1
 #endif
+template <int KIND>
+__host__ __device__ constexpr int fill_form() { return SQ_FILL_FORM >= 0 ? SQ_FILL_FORM : (KIND == KIND_U32 ? 3 : 0); }
 template <int KIND, int FORM>
 __device__ __forceinline__ void put(uint32_t (&v)[16], int j, uint64_t y, uint64_t z, uint64_t u, uint32_t one) {
   if (KIND == KIND_U32 || KIND == KIND_F32) {
@@ -106,7 +110,7 @@ __device__ __forceinline__ void gen_lane(const State& s, const RowConst<SPL>& rc
 #else
     const uint64_t z = add64(y, rc.key);
 #endif
-    put<KIND, SQ_FILL_FORM>(v, j, y, z, u, one);
+    put<KIND, fill_form<KIND>()>(v, j, y, z, u, one);
     if (j < SPL - 1) {
       y = STRIDED ? add64(y, rc.K) : z;
       u = j ? add64_3(u, s.e, rc.cst[j]) : add64(u, s.e);

@@ -7,15 +7,13 @@
 //  * One CTA of 1024 threads per SM (persistent), each thread owning one contiguous counter
 //    range, walked with the multiply-free Weyl/finite-difference step (squares_device.cuh).
 //  * hist: a 65536-bin histogram held in shared memory as 16-bit counters packed two per
-//    32-bit word (128 KiB; 32-bit bins would need 256 KiB > 227 KiB).  Exactness by a
-//    guard-bit + epoch scheme: a CTA barrier follows every 32 samples per thread, so at most
-//    1024*32 = 0x8000 increments reach any half per epoch; every half is <= 0x7FFF at an
-//    epoch start, so it never exceeds 0xFFFF (no carry into its neighbour).  The one thread
-//    whose ATOMS.ADD moves a half from 0x7FFF to 0x8000 (seen in the returned old value)
-//    subtracts 0x8000 from that half and adds 0x8000 to the global bin before the next
-//    barrier, restoring the invariant.  Final bin = sum of fix-ups + residual.
+//    32-bit word (128 KiB; 32-bit bins would need 256 KiB > 227 KiB).  Exact by the sweep
+//    scheme of hist16.cuh: a CTA barrier follows every 32 samples per thread (<= 0x8000
+//    increments per epoch); each ATOMS's old word is ORed into a per-thread flag word, and
+//    the CTA sweeps all bins to global memory at a barrier where some half was seen >= 0x4000,
+//    so every half stays <= 0xC000.  No per-sample branch on an ATOMS result.
 //  * ones[16..31] are derived exactly from the histogram (bit j of u is bit j-16 of its bin):
-//    from the CTA's residual bins and its fix-ups, at the end.
+//    from the bins each sweep (and the final flush) moves to global memory.
 //  * ones[0..15]: bit-sliced carry-save counting.  Two samples' low halves are packed in one
 //    32-bit word (columns j and j+16 both count bit j); a Harley-Seal tree folds 16 words
 //    (one epoch) into a weight-16 word, which is ripple-added into 6 vertical counter planes,
@@ -37,9 +35,9 @@ constexpr int kFlushEvery = 63 / kTrees;          // epochs between plane flushe
 constexpr int kWordsPerThread = 32768 / kFusedThreads;
 constexpr int kLogW = (kWordsPerThread == 32) ? 5 : 6;
 static_assert(kEpoch % 32 == 0 && (1 << kLogW) == kWordsPerThread, "fused geometry");
-constexpr size_t kFusedSmem = 32768 * 4 + 16 * 8 + 16 * 8 + 16 * 4;
+constexpr size_t kFusedSmem = 32768 * 4 + 16 * 8 + 16 * 8;
 
-static_assert(kFusedThreads * kEpoch <= 0x8000, "epoch bound of the guard-bit scheme");
+static_assert(kFusedThreads * kEpoch <= kSweepEpochIncs, "epoch bound of the sweep scheme");
 
 // carry-save adder: (h, l) = (maj(a,b,c), a^b^c)
 __device__ __forceinline__ void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32_t b, uint32_t c) {
@@ -75,14 +73,17 @@ struct WalkConst {
 // u(c+j+1) = u(c+j) + e(c) + j*2k^2 (squares_device.cuh), e advances once per group.
 // STRIDED: counters advance by `stride` (y by K, z = y + key separately); BITREV: each
 // output is bit-reversed before it is counted ("bits-reversed tests").
+#ifndef SQ_FUSED_FORM
+#define SQ_FUSED_FORM 0
+#endif
 template <bool STRIDED, bool BITREV>
 __device__ __forceinline__ void gen8(State& s, const WalkConst& wc, uint32_t (&v)[8], uint32_t one) {
   uint64_t y = s.y, u = s.u;
 #pragma unroll
   for (int j = 0; j < 8; j++) {
     const uint64_t z = add64(y, wc.key);
-    // FORM 1 (doubling as a variable shift, ALU pipe): +3.5 % here on B200
-    const uint32_t o = squares32_from<1>(y, z, u, one);
+    // FORM 0 (plain doubling) measured fastest with the sweep scheme (991 vs 947 Gs/s FORM 1)
+    const uint32_t o = squares32_from<SQ_FUSED_FORM>(y, z, u, one);
     v[j] = BITREV ? __brev(o) : o;
     y = STRIDED ? add64(y, wc.K) : z;
     u = j ? add64_3(u, s.e, wc.cst[j]) : add64(u, s.e);
@@ -92,23 +93,22 @@ __device__ __forceinline__ void gen8(State& s, const WalkConst& wc, uint32_t (&v
   s.e = add64(s.e, wc.cst8);
 }
 
-// Histogram updates for 8 samples (masked ones skipped) and their packed low halves:
+// Histogram updates for 8 samples (masked ones add 0) and their packed low halves:
 // w[i] = low half of v[2i] | low half of v[2i+1] << 16 (masked samples contribute 0).
+// The ATOMS results only feed the sweep vote (acc), so the 8 updates issue back to back.
 template <bool MASKED>
-__device__ __forceinline__ void reduce8(const uint32_t (&v)[8], uint32_t (&w)[4], uint32_t* bins,
-                                        unsigned long long* hist, uint32_t* fix, int64_t base_rem) {
+__device__ __forceinline__ void reduce8(const uint32_t (&v)[8], uint32_t (&w)[4], uint32_t* bins, uint32_t& acc,
+                                        int64_t base_rem) {
 #pragma unroll
   for (int i = 0; i < 4; i++) {
     uint32_t a = v[2 * i], b = v[2 * i + 1];
     if (MASKED) {
       const bool va = base_rem > 2 * i, vb = base_rem > 2 * i + 1;
-      hist_add<true>(bins, a, hist, fix, va);
-      hist_add<true>(bins, b, hist, fix, vb);
+      acc |= hist_add_sweep(bins, a, va) | hist_add_sweep(bins, b, vb);
       if (!va) a = 0;
       if (!vb) b = 0;
     } else {
-      hist_add<true>(bins, a, hist, fix);
-      hist_add<true>(bins, b, hist, fix);
+      acc |= hist_add_sweep(bins, a) | hist_add_sweep(bins, b);
     }
     w[i] = __byte_perm(a, b, 0x5410);
   }
@@ -117,9 +117,8 @@ __device__ __forceinline__ void reduce8(const uint32_t (&v)[8], uint32_t (&w)[4]
 // One epoch (32 samples = 16 packed words) folded by Harley-Seal into a weight-16 word.
 template <bool MASKED, bool STRIDED, bool BITREV>
 __device__ __forceinline__ uint32_t epoch(State& s, const WalkConst& wc, uint32_t one, uint32_t* bins,
-                                          unsigned long long* hist, uint32_t* fix, int64_t rem,
-                                          uint32_t& ones, uint32_t& twos, uint32_t& fours,
-                                          uint32_t& eights) {
+                                          uint32_t& acc, int64_t rem, uint32_t& ones, uint32_t& twos,
+                                          uint32_t& fours, uint32_t& eights) {
   uint32_t eightsAB[2];
 #pragma unroll
   for (int blk = 0; blk < 2; blk++) {
@@ -128,7 +127,7 @@ __device__ __forceinline__ uint32_t epoch(State& s, const WalkConst& wc, uint32_
     for (int h = 0; h < 2; h++) {
       uint32_t v[8], w[4], twosA, twosB;
       gen8<STRIDED, BITREV>(s, wc, v, one);
-      reduce8<MASKED>(v, w, bins, hist, fix, rem - 8 * (2 * blk + h));
+      reduce8<MASKED>(v, w, bins, acc, rem - 8 * (2 * blk + h));
       csa(twosA, ones, ones, w[0], w[1]);
       csa(twosB, ones, ones, w[2], w[3]);
       csa(foursAB[h], twos, twos, twosA, twosB);
@@ -140,6 +139,39 @@ __device__ __forceinline__ uint32_t epoch(State& s, const WalkConst& wc, uint32_
   return sixteens;
 }
 
+// Moves every bin of the CTA's shared histogram to the global histogram and zeroes it (a
+// sweep, or the final flush), adding the moved counts per set bin bit into hi_cnt[0..15]
+// (ones[16 + j] counts bit j of the bin).  Thread tid owns words [W*tid, W*tid+W)
+// (W = kWordsPerThread) = bins [2W*tid, 2W*tid+2W): a bin's bit 0 is the half, bits 1..kLogW
+// the word index i (visited rotated by lane: conflict-free banks), the higher bits are tid's.
+// Called by all threads between barriers (no concurrent ATOMS).
+__device__ __noinline__ void flush_bins(uint32_t* bins, unsigned long long* hist, unsigned long long* hi_cnt) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  uint32_t T = 0, S[kLogW + 1];
+#pragma unroll
+  for (int j = 0; j <= kLogW; j++) S[j] = 0;
+#pragma unroll 4
+  for (uint32_t k = 0; k < kWordsPerThread; k++) {
+    const uint32_t i = (k + lane) & (kWordsPerThread - 1);
+    const uint32_t wv = bins[kWordsPerThread * tid + i];
+    if (!wv) continue;
+    bins[kWordsPerThread * tid + i] = 0;
+    const uint32_t lo = wv & 0xFFFFu, hi = wv >> 16;
+    const uint32_t b0 = 2 * kWordsPerThread * tid + 2 * i;
+    if (lo) atomicAdd(&hist[b0], (unsigned long long)lo);
+    if (hi) atomicAdd(&hist[b0 + 1], (unsigned long long)hi);
+    T += lo + hi;   // <= 2W * 0xFFFF < 2^32
+    S[0] += hi;
+#pragma unroll
+    for (int j = 1; j <= kLogW; j++) S[j] += ((i >> (j - 1)) & 1u) ? (lo + hi) : 0u;
+  }
+  uint32_t colcnt[16];
+#pragma unroll
+  for (int j = 0; j < 16; j++)
+    colcnt[j] = (j <= kLogW) ? S[j] : (((tid >> (j - 1 - kLogW)) & 1u) ? T : 0u);
+  warp_flush16(colcnt, hi_cnt);
+}
+
 template <bool STRIDED, bool BITREV>
 __global__ void __launch_bounds__(kFusedThreads, 1)
 fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t r, uint32_t epochs,
@@ -148,10 +180,9 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
   uint32_t* bins = smem;
   unsigned long long* lo_cnt = (unsigned long long*)(smem + 32768);
   unsigned long long* hi_cnt = lo_cnt + 16;
-  uint32_t* fix = (uint32_t*)(hi_cnt + 16);
   const uint32_t tid = threadIdx.x;
   for (uint32_t i = tid; i < 32768; i += kFusedThreads) bins[i] = 0;
-  if (tid < 16) { lo_cnt[tid] = 0; hi_cnt[tid] = 0; fix[tid] = 0; }
+  if (tid < 16) { lo_cnt[tid] = 0; hi_cnt[tid] = 0; }
   __syncthreads();
 
   const uint64_t t = (uint64_t)blockIdx.x * kFusedThreads + tid;
@@ -181,14 +212,15 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
   uint64_t done = 0;
   int since_flush = 0;
   for (uint32_t ep = 0; ep < epochs; ep++) {
+    uint32_t acc = 0;
 #pragma unroll
     for (int tr = 0; tr < kTrees; tr++) {
       uint32_t sixteens;
       if (done + 32 <= cnt) {
-        sixteens = epoch<false, STRIDED, BITREV>(s, wc, one, bins, hist, fix, 32, ones, twos, fours, eights);
+        sixteens = epoch<false, STRIDED, BITREV>(s, wc, one, bins, acc, 32, ones, twos, fours, eights);
       } else {
         const int64_t rem = done < cnt ? (int64_t)(cnt - done) : 0;
-        sixteens = epoch<true, STRIDED, BITREV>(s, wc, one, bins, hist, fix, rem, ones, twos, fours, eights);
+        sixteens = epoch<true, STRIDED, BITREV>(s, wc, one, bins, acc, rem, ones, twos, fours, eights);
       }
       done += 32;
       // ripple-add the weight-16 word into the vertical planes
@@ -206,7 +238,11 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
       for (int p = 0; p < kPlanes; p++) { columns_add(colcnt, pl[p], 16u << p); pl[p] = 0; }
       warp_flush16(colcnt, lo_cnt);
     }
-    __syncthreads();   // epoch boundary of the guard-bit scheme
+    // epoch boundary of the sweep scheme (hist16.cuh): vote, and sweep if any half got hot
+    if (__syncthreads_or((acc & kSweepMask) != 0)) {
+      flush_bins(bins, hist, hi_cnt);
+      __syncthreads();
+    }
   }
   // remaining carry-save state: weights 1, 2, 4, 8 and the planes
   columns_add(colcnt, ones, 1);
@@ -217,35 +253,11 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
   for (int p = 0; p < kPlanes; p++) columns_add(colcnt, pl[p], 16u << p);
   warp_flush16(colcnt, lo_cnt);
 
-  // residual bins -> global hist; bits 16..31 derived from the residual bins.
-  // Thread tid owns words [W*tid, W*tid+W) (W = kWordsPerThread) = bins [2W*tid, 2W*tid+2W):
-  // a bin's bit 0 is the half, bits 1..kLogW the word index i (rotated by lane for
-  // conflict-free banks), and the higher bits are tid's bits.
-  uint32_t T = 0, S[kLogW + 1];
-#pragma unroll
-  for (int j = 0; j <= kLogW; j++) S[j] = 0;
-  const uint32_t lane = tid & 31;
-#pragma unroll 4
-  for (uint32_t k = 0; k < kWordsPerThread; k++) {
-    const uint32_t i = (k + lane) & (kWordsPerThread - 1);
-    const uint32_t wv = bins[kWordsPerThread * tid + i];
-    const uint32_t lo = wv & 0xFFFFu, hi = wv >> 16;
-    const uint32_t b0 = 2 * kWordsPerThread * tid + 2 * i;
-    if (lo) atomicAdd(&hist[b0], (unsigned long long)lo);
-    if (hi) atomicAdd(&hist[b0 + 1], (unsigned long long)hi);
-    T += lo + hi;
-    S[0] += hi;
-#pragma unroll
-    for (int j = 1; j <= kLogW; j++) S[j] += ((i >> (j - 1)) & 1u) ? (lo + hi) : 0u;
-  }
-#pragma unroll
-  for (int j = 0; j < 16; j++)
-    colcnt[j] = (j <= kLogW) ? S[j] : (((tid >> (j - 1 - kLogW)) & 1u) ? T : 0u);
-  warp_flush16(colcnt, hi_cnt);
+  // residual bins -> global hist (bits 16..31 derived from them)
+  flush_bins(bins, hist, hi_cnt);
   __syncthreads();
   if (tid < 16) {
-    const unsigned long long lo = lo_cnt[tid];
-    const unsigned long long hi = hi_cnt[tid] + 0x8000ull * (unsigned long long)fix[tid];
+    const unsigned long long lo = lo_cnt[tid], hi = hi_cnt[tid];
     if (lo) atomicAdd(&ones_out[tid], lo);
     if (hi) atomicAdd(&ones_out[16 + tid], hi);
   }

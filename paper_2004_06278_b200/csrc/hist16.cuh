@@ -42,3 +42,32 @@ __device__ __forceinline__ void hist_add(uint32_t* bins, uint32_t v, unsigned lo
 }
 
 }  // namespace sq
+
+namespace sq {
+
+// ---------------------------------------------------------------------------------------
+// Sweep scheme (fused statistics): the same packed 16-bit bins, exact by a THRESHOLD
+// invariant instead of a per-sample fix-up, so the hot loop never branches on an ATOMS result.
+//
+// Contract: a CTA barrier separates epochs and at most kSweepEpochIncs increments reach any
+// half per epoch.  Invariant I: every half <= kSweepT (0x4000) at an epoch start.  Each thread
+// ORs the OLD word returned by each of its ATOMS into `acc`; at the epoch barrier the CTA
+// votes (__syncthreads_or) on (acc & 0xC000C000) -- "some half was seen at >= 0x4000 before an
+// increment".  No vote => every increment found its half < 0x4000, so every half ends the
+// epoch <= 0x4000 and I holds.  A vote => the CTA sweeps all bins to the global histogram
+// (every half -> 0), so I holds again.  Overflow: a half starts <= 0x4000 and gains <= 0x8000
+// within an epoch, so it stays <= 0xC000 < 0x10000 and never carries into its neighbour.
+// The other half of a returned word only causes extra (harmless) sweeps.  With near-uniform
+// bins a sweep happens about once per 2^30 samples per CTA.
+constexpr uint32_t kSweepT = 0x4000;
+constexpr uint32_t kSweepMask = 0xC000C000u;   // bits >= 0x4000 of both halves
+constexpr uint32_t kSweepEpochIncs = 0x8000;   // per-epoch increment bound per CTA
+
+// Bin (v >> 16) += 1 (or += 0 for a masked lane); returns the old word for the vote.
+__device__ __forceinline__ uint32_t hist_add_sweep(uint32_t* bins, uint32_t v, bool valid = true) {
+  uint32_t inc = (v & 0x10000u) ? 0x10000u : 1u;
+  if (!valid) inc = 0;
+  return atomicAdd(&bins[v >> 17], inc);
+}
+
+}  // namespace sq

@@ -198,8 +198,9 @@ def test_fused_accumulates(sq):
 
 
 def test_fused_key_zero_guard_path(sq):
-    """key = 0: every sample lands in bin 0, driving the guard-bit fix-up path ~2^24/2^15 times
-    per CTA; closed form hist[0] = n, ones = 0."""
+    """key = 0: every sample lands in bin 0, so the shared-memory histogram is swept to global
+    memory at almost every epoch barrier (hist16.cuh sweep scheme); closed form hist[0] = n,
+    ones = 0."""
     n = 1 << 26
     h, o = _fused(sq, 0, 5, n)
     assert h[0] == n and h[1:].sum() == 0 and o.sum() == 0
@@ -207,7 +208,7 @@ def test_fused_key_zero_guard_path(sq):
 
 def test_fused_hot_bins_both_halves(sq):
     """key = 2^32: outputs concentrate on few bins for small counters (closed form family);
-    checks fix-ups in both 16-bit halves against the oracle."""
+    checks sweeps of hot bins in both 16-bit halves against the oracle."""
     n = 1 << 23
     h, o = _fused(sq, 1 << 32, 0, n)
     hw, ow = O.fused_stats(1 << 32, 0, n)
