@@ -122,6 +122,16 @@ __device__ __forceinline__ uint32_t squares32_from(uint64_t y, uint64_t z, uint6
   return round_hi<FORM>(xh, xl, z, one);  // round 4
 }
 
+// squares32 with a cross-term form per round (F2, F3, F4 for rounds 2, 3, 4): lets a kernel
+// balance the doublings between the ALU and FMA pipes.  Same result as squares32_from.
+template <int F2, int F3, int F4>
+__device__ __forceinline__ uint32_t squares32_mix(uint64_t y, uint64_t z, uint64_t u, uint32_t one = 1) {
+  uint32_t xh = lo32(u), xl = hi32(u);
+  round_rot<F2>(xh, xl, z, one);
+  round_rot<F3>(xh, xl, y, one);
+  return round_hi<F4>(xh, xl, z, one);
+}
+
 // squares64 given y, z, u as above.  P:56-64: t = x*x + z (round 4, kept before rotating),
 // result t ^ ((rot32(t)^2 + y) >> 32); only t's low half changes.
 template <int FORM = SQ_ROUND_FORM>

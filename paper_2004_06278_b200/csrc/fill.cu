@@ -39,7 +39,7 @@ __device__ __forceinline__ void st256(void* p, const uint32_t* v) {
 // the in-chunk 3-input u step.
 template <int SPL>
 struct RowConst {
-  uint64_t key, K, jk, cj, dj;
+  uint64_t key, K, jk, cj, dj, k2x2;
   uint64_t cst[SPL];
 };
 
@@ -54,6 +54,7 @@ __device__ __forceinline__ RowConst<SPL> row_const(uint64_t key, uint64_t stride
   rc.jk = J * K;
   rc.cj = J * (J - 1) * K * K;
   rc.dj = J * k2x2;
+  rc.k2x2 = k2x2;
   rc.cst[0] = 0;
 #pragma unroll
   for (int j = 1; j < SPL; j++) rc.cst[j] = rc.cst[j - 1] + k2x2;
@@ -71,7 +72,11 @@ __host__ __device__ constexpr int fill_form() { return SQ_FILL_FORM >= 0 ? SQ_FI
 template <int KIND, int FORM>
 __device__ __forceinline__ void put(uint32_t (&v)[16], int j, uint64_t y, uint64_t z, uint64_t u, uint32_t one) {
   if (KIND == KIND_U32 || KIND == KIND_F32) {
+#ifdef SQ_FILL_MIX2
+    const uint32_t o = (KIND == KIND_U32) ? squares32_mix<SQ_FILL_MIX2, SQ_FILL_MIX3, SQ_FILL_MIX4>(y, z, u, one) : squares32_from<FORM>(y, z, u, one);
+#else
     const uint32_t o = squares32_from<FORM>(y, z, u, one);
+#endif
     v[j] = (KIND == KIND_F32) ? __float_as_uint(u32_to_unit_f32(o)) : o;
   } else {
     const uint64_t o = squares64_from<FORM>(y, z, u, one);
@@ -92,12 +97,15 @@ __device__ __forceinline__ void put(uint32_t (&v)[16], int j, uint64_t y, uint64
 // The SPL outputs of one lane from state s (not modified).  Consecutive counters
 // (STRIDED = false): z = y + key is the next counter's y.  Strided: y steps by K and
 // z = y + key separately (one more 64-bit add per sample).
+#ifndef SQ_FILL_CHAIN2
+#define SQ_FILL_CHAIN2 0
+#endif
 #ifndef SQ_FILL_Y3
 #define SQ_FILL_Y3 0
 #endif
-template <int KIND, int SPL, bool STRIDED>
+template <int KIND, int SPL, bool STRIDED, bool CHAIN2 = false>
 __device__ __forceinline__ void gen_lane(const State& s, const RowConst<SPL>& rc, uint32_t (&v)[16], uint32_t one) {
-  uint64_t y = s.y, u = s.u;
+  uint64_t y = s.y, u = s.u, e = s.e;
 #if SQ_FILL_Y3
   // y + key as a 3-input add y + (key - one) + one with the opaque one: IMAD cannot express a
   // 3-input add, so both halves stay on the ALU pipe (IADD3 / IADD3.X with two carries)
@@ -113,7 +121,12 @@ __device__ __forceinline__ void gen_lane(const State& s, const RowConst<SPL>& rc
     put<KIND, fill_form<KIND>()>(v, j, y, z, u, one);
     if (j < SPL - 1) {
       y = STRIDED ? add64(y, rc.K) : z;
-      u = j ? add64_3(u, s.e, rc.cst[j]) : add64(u, s.e);
+      if (CHAIN2) {   // u += e; e += 2K^2: no per-row constant table (fewer registers)
+        u = add64(u, e);
+        e = add64(e, rc.k2x2);
+      } else {
+        u = j ? add64_3(u, s.e, rc.cst[j]) : add64(u, s.e);
+      }
     }
   }
 }
@@ -164,7 +177,7 @@ __global__ void __launch_bounds__(kFillThreads, KEYIMM ? kFillMinBlocksImm : kFi
         i0 += nfull * J;
         cc += nfull;
         for (; nfull; nfull--) {
-          gen_lane<KIND, SPL, STRIDED>(s, rc, v, a.one);
+          gen_lane<KIND, SPL, STRIDED, SQ_FILL_CHAIN2 && !KEYIMM>(s, rc, v, a.one);
 #ifdef SQ_FILL_NOSTORE   // experiment: generation without the output stream
 #pragma unroll
           for (int j = 0; j < 16; j++) nostore_acc ^= v[j];
@@ -177,7 +190,7 @@ __global__ void __launch_bounds__(kFillThreads, KEYIMM ? kFillMinBlocksImm : kFi
         }
       } else {
         // boundary chunk (row head or ragged tail): per-element masked stores
-        gen_lane<KIND, SPL, STRIDED>(s, rc, v, a.one);
+        gen_lane<KIND, SPL, STRIDED, SQ_FILL_CHAIN2 && !KEYIMM>(s, rc, v, a.one);
         char* p = rowp + (int64_t)i0 * ES;
 #pragma unroll
         for (int j = 0; j < SPL; j++) {

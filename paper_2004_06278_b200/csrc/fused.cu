@@ -83,7 +83,11 @@ __device__ __forceinline__ void gen8(State& s, const WalkConst& wc, uint32_t (&v
   for (int j = 0; j < 8; j++) {
     const uint64_t z = add64(y, wc.key);
     // FORM 0 (plain doubling) measured fastest with the sweep scheme (991 vs 947 Gs/s FORM 1)
+#ifdef SQ_FUSED_MIX2
+    const uint32_t o = squares32_mix<SQ_FUSED_MIX2, SQ_FUSED_MIX3, SQ_FUSED_MIX4>(y, z, u, one);
+#else
     const uint32_t o = squares32_from<SQ_FUSED_FORM>(y, z, u, one);
+#endif
     v[j] = BITREV ? __brev(o) : o;
     y = STRIDED ? add64(y, wc.K) : z;
     u = j ? add64_3(u, s.e, wc.cst[j]) : add64(u, s.e);
