@@ -73,6 +73,9 @@ struct WalkConst {
 // u(c+j+1) = u(c+j) + e(c) + j*2k^2 (squares_device.cuh), e advances once per group.
 // STRIDED: counters advance by `stride` (y by K, z = y + key separately); BITREV: each
 // output is bit-reversed before it is counted ("bits-reversed tests").
+#ifndef SQ_FUSED_PIPE
+#define SQ_FUSED_PIPE 1
+#endif
 #ifndef SQ_FUSED_FORM
 #define SQ_FUSED_FORM 0
 #endif
@@ -102,17 +105,17 @@ __device__ __forceinline__ void gen8(State& s, const WalkConst& wc, uint32_t (&v
 // The ATOMS results only feed the sweep vote (acc), so the 8 updates issue back to back.
 template <bool MASKED>
 __device__ __forceinline__ void reduce8(const uint32_t (&v)[8], uint32_t (&w)[4], uint32_t* bins, uint32_t& acc,
-                                        int64_t base_rem) {
+                                        int64_t base_rem, uint32_t one) {
 #pragma unroll
   for (int i = 0; i < 4; i++) {
     uint32_t a = v[2 * i], b = v[2 * i + 1];
     if (MASKED) {
       const bool va = base_rem > 2 * i, vb = base_rem > 2 * i + 1;
-      acc |= hist_add_sweep(bins, a, va) | hist_add_sweep(bins, b, vb);
+      acc |= hist_add_sweep(bins, a, one, va) | hist_add_sweep(bins, b, one, vb);
       if (!va) a = 0;
       if (!vb) b = 0;
     } else {
-      acc |= hist_add_sweep(bins, a) | hist_add_sweep(bins, b);
+      acc |= hist_add_sweep(bins, a, one) | hist_add_sweep(bins, b, one);
     }
     w[i] = __byte_perm(a, b, 0x5410);
   }
@@ -123,21 +126,37 @@ template <bool MASKED, bool STRIDED, bool BITREV>
 __device__ __forceinline__ uint32_t epoch(State& s, const WalkConst& wc, uint32_t one, uint32_t* bins,
                                           uint32_t& acc, int64_t rem, uint32_t& ones, uint32_t& twos,
                                           uint32_t& fours, uint32_t& eights) {
-  uint32_t eightsAB[2];
+  uint32_t eightsAB[2], foursAB[2];
+#if SQ_FUSED_PIPE
+  // generation one 8-sample batch ahead of the reduction (software pipelined source order)
+  uint32_t vb[2][8];
+  gen8<STRIDED, BITREV>(s, wc, vb[0], one);
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const int blk = k >> 1, h = k & 1;
+    if (k < 3) gen8<STRIDED, BITREV>(s, wc, vb[(k + 1) & 1], one);
+    uint32_t w[4], twosA, twosB;
+    reduce8<MASKED>(vb[k & 1], w, bins, acc, rem - 8 * k, one);
+    csa(twosA, ones, ones, w[0], w[1]);
+    csa(twosB, ones, ones, w[2], w[3]);
+    csa(foursAB[h], twos, twos, twosA, twosB);
+    if (h) csa(eightsAB[blk], fours, fours, foursAB[0], foursAB[1]);
+  }
+#else
 #pragma unroll
   for (int blk = 0; blk < 2; blk++) {
-    uint32_t foursAB[2];
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       uint32_t v[8], w[4], twosA, twosB;
       gen8<STRIDED, BITREV>(s, wc, v, one);
-      reduce8<MASKED>(v, w, bins, acc, rem - 8 * (2 * blk + h));
+      reduce8<MASKED>(v, w, bins, acc, rem - 8 * (2 * blk + h), one);
       csa(twosA, ones, ones, w[0], w[1]);
       csa(twosB, ones, ones, w[2], w[3]);
       csa(foursAB[h], twos, twos, twosA, twosB);
     }
     csa(eightsAB[blk], fours, fours, foursAB[0], foursAB[1]);
   }
+#endif
   uint32_t sixteens;
   csa(sixteens, eights, eights, eightsAB[0], eightsAB[1]);
   return sixteens;
@@ -160,7 +179,8 @@ __device__ __noinline__ void flush_bins(uint32_t* bins, unsigned long long* hist
     const uint32_t wv = bins[kWordsPerThread * tid + i];
     if (!wv) continue;
     bins[kWordsPerThread * tid + i] = 0;
-    const uint32_t lo = wv & 0xFFFFu, hi = wv >> 16;
+    uint32_t lo, hi;   // counts of bins b0 and b0 + 1
+    sweep_word_counts(wv, lo, hi);
     const uint32_t b0 = 2 * kWordsPerThread * tid + 2 * i;
     if (lo) atomicAdd(&hist[b0], (unsigned long long)lo);
     if (hi) atomicAdd(&hist[b0 + 1], (unsigned long long)hi);

@@ -215,6 +215,23 @@ def test_fused_hot_bins_both_halves(sq):
     assert np.array_equal(h, hw) and np.array_equal(o, ow)
 
 
+@pytest.mark.parametrize("key", [1 << 32, (1 << 32) + (1 << 16)])
+def test_fused_hot_bins_accumulate_in_pieces(sq, key):
+    """Hot bins (closed-form key family) counted in three pieces into the same non-zero arrays:
+    the sweeps of each piece (A/B word packing of hist16.cuh, derived ones[16..31]) must add up
+    to the single-run oracle."""
+    n = (1 << 23) + 12345
+    h = torch.zeros(65536, dtype=torch.int64, device="cuda")
+    o = torch.zeros(32, dtype=torch.int64, device="cuda")
+    cuts = [0, 1 << 21, (1 << 21) + 777, n]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        sq.fused_stats(key, 3 + a, b - a, h, o)
+    torch.cuda.synchronize()
+    hw, ow = O.fused_stats(key, 3, n)
+    assert np.array_equal(h.cpu().numpy().view(np.uint64), hw)
+    assert np.array_equal(o.cpu().numpy().view(np.uint64), ow)
+
+
 def test_fused_2_30_vs_parallel_oracle(sq):
     key = int(O.keygen(1, 1)[0])
     n = 1 << 30
