@@ -21,6 +21,9 @@ from . import dist  # noqa: F401  (multi-GPU composition: partition + NCCL all-r
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsquares.so")
+# SQ_LIB: load an experimental build of the same library instead (tools/build_variant.sh);
+# unset for the product path.
+LIB_PATH = os.environ.get("SQ_LIB", LIB_PATH)
 
 SQ_OK, SQ_EINVAL, SQ_ERANGE, SQ_ECUDA, SQ_ENOMEM = 0, 1, 2, 3, 4
 KEY_UPPER_REPEAT, KEY_LOWER_REPEAT, KEY_ZERO_DIGIT, KEY_EVEN, KEY_POPCOUNT = 1, 2, 4, 8, 16

@@ -28,16 +28,22 @@
 
 namespace sq {
 
-constexpr int kEpoch = 0x8000 / kFusedThreads;   // samples per thread per epoch (x threads = 0x8000)
+// Geometry: kFusedThreads threads per CTA (one CTA per SM), kEpoch samples per thread between
+// barriers, so at most kFusedThreads * kEpoch increments per epoch; the sweep threshold is the
+// largest power of two T with T + increments <= 0xFFFF (hist16.cuh).
+#ifndef SQ_FUSED_EPOCH
+#define SQ_FUSED_EPOCH (0x8000 / SQ_FUSED_THREADS)
+#endif
+constexpr int kEpoch = SQ_FUSED_EPOCH;
+constexpr uint32_t kEpochIncs = (uint32_t)kFusedThreads * kEpoch;
+constexpr uint32_t kT = sweep_threshold(kEpochIncs);
+constexpr uint32_t kMask = sweep_mask(kT);
 constexpr int kTrees = kEpoch / 32;               // 16-word Harley-Seal trees per epoch
 constexpr int kPlanes = 6;                        // vertical planes for weight-16 words: counts up to 63
 constexpr int kFlushEvery = 63 / kTrees;          // epochs between plane flushes
-constexpr int kWordsPerThread = 32768 / kFusedThreads;
-constexpr int kLogW = (kWordsPerThread == 32) ? 5 : 6;
-static_assert(kEpoch % 32 == 0 && (1 << kLogW) == kWordsPerThread, "fused geometry");
+static_assert(kEpoch % 32 == 0 && kTrees >= 1, "fused geometry");
+static_assert(kT >= 0x100 && kT + kEpochIncs <= 0xFFFFu, "epoch bound of the sweep scheme");
 constexpr size_t kFusedSmem = 32768 * 4 + 16 * 8 + 16 * 8;
-
-static_assert(kFusedThreads * kEpoch <= kSweepEpochIncs, "epoch bound of the sweep scheme");
 
 // carry-save adder: (h, l) = (maj(a,b,c), a^b^c)
 __device__ __forceinline__ void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32_t b, uint32_t c) {
@@ -164,35 +170,27 @@ __device__ __forceinline__ uint32_t epoch(State& s, const WalkConst& wc, uint32_
 
 // Moves every bin of the CTA's shared histogram to the global histogram and zeroes it (a
 // sweep, or the final flush), adding the moved counts per set bin bit into hi_cnt[0..15]
-// (ones[16 + j] counts bit j of the bin).  Thread tid owns words [W*tid, W*tid+W)
-// (W = kWordsPerThread) = bins [2W*tid, 2W*tid+2W): a bin's bit 0 is the half, bits 1..kLogW
-// the word index i (visited rotated by lane: conflict-free banks), the higher bits are tid's.
-// Called by all threads between barriers (no concurrent ATOMS).
+// (ones[16 + j] counts bit j of the bin: bit 0 is the word's odd bin, bits 1..15 the word
+// index).  Thread tid visits words tid, tid + T, ... (conflict-free banks).  Rare (the final
+// flush plus about one sweep per 2^29 samples per CTA), so it favours simplicity.  Called by
+// all threads between barriers (no concurrent ATOMS).
 __device__ __noinline__ void flush_bins(uint32_t* bins, unsigned long long* hist, unsigned long long* hi_cnt) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31;
-  uint32_t T = 0, S[kLogW + 1];
-#pragma unroll
-  for (int j = 0; j <= kLogW; j++) S[j] = 0;
-#pragma unroll 4
-  for (uint32_t k = 0; k < kWordsPerThread; k++) {
-    const uint32_t i = (k + lane) & (kWordsPerThread - 1);
-    const uint32_t wv = bins[kWordsPerThread * tid + i];
-    if (!wv) continue;
-    bins[kWordsPerThread * tid + i] = 0;
-    uint32_t lo, hi;   // counts of bins b0 and b0 + 1
-    sweep_word_counts(wv, lo, hi);
-    const uint32_t b0 = 2 * kWordsPerThread * tid + 2 * i;
-    if (lo) atomicAdd(&hist[b0], (unsigned long long)lo);
-    if (hi) atomicAdd(&hist[b0 + 1], (unsigned long long)hi);
-    T += lo + hi;   // <= 2W * 0xFFFF < 2^32
-    S[0] += hi;
-#pragma unroll
-    for (int j = 1; j <= kLogW; j++) S[j] += ((i >> (j - 1)) & 1u) ? (lo + hi) : 0u;
-  }
   uint32_t colcnt[16];
 #pragma unroll
-  for (int j = 0; j < 16; j++)
-    colcnt[j] = (j <= kLogW) ? S[j] : (((tid >> (j - 1 - kLogW)) & 1u) ? T : 0u);
+  for (int j = 0; j < 16; j++) colcnt[j] = 0;
+  for (uint32_t w = threadIdx.x; w < 32768; w += blockDim.x) {
+    const uint32_t wv = bins[w];
+    if (!wv) continue;
+    bins[w] = 0;
+    uint32_t lo, hi;   // counts of bins 2w and 2w + 1 (each <= 0xFFFF)
+    sweep_word_counts(wv, lo, hi);
+    if (lo) atomicAdd(&hist[2 * w], (unsigned long long)lo);
+    if (hi) atomicAdd(&hist[2 * w + 1], (unsigned long long)hi);
+    colcnt[0] += hi;
+#pragma unroll
+    for (int j = 1; j < 16; j++) colcnt[j] += ((w >> (j - 1)) & 1u) ? (lo + hi) : 0u;
+  }
+  // per thread <= 43 words x 0x1FFFE per flush: no 32-bit overflow before warp_flush16
   warp_flush16(colcnt, hi_cnt);
 }
 
@@ -263,7 +261,7 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
       warp_flush16(colcnt, lo_cnt);
     }
     // epoch boundary of the sweep scheme (hist16.cuh): vote, and sweep if any half got hot
-    if (__syncthreads_or((acc & kSweepMask) != 0)) {
+    if (__syncthreads_or((acc & kMask) != 0)) {
       flush_bins(bins, hist, hi_cnt);
       __syncthreads();
     }

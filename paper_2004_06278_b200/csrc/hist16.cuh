@@ -54,8 +54,8 @@ namespace sq {
 // predicate + SEL, or a single LOP3 `(v & 0x10000) | 1` -- and bin 2w = A - B, bin 2w+1 = B at
 // flush time.
 //
-// Contract: a CTA barrier separates epochs and at most kSweepEpochIncs increments reach any
-// word per epoch.  Invariant I: A <= kSweepT (0x4000) in every word at an epoch start (B <= A).
+// Contract: a CTA barrier separates epochs and at most 0x8000 increments reach any word per
+// epoch.  Invariant I: A <= T = 0x4000 in every word at an epoch start (B <= A).
 // Each thread ORs the OLD word returned by each of its ATOMS into `acc`; at the epoch barrier
 // the CTA votes (__syncthreads_or) on (acc & 0xC000C000) -- "some A (or B) was seen at >= 0x4000
 // before an increment".  No vote => every increment found A < 0x4000, so every A ends the epoch
@@ -63,9 +63,16 @@ namespace sq {
 // word -> 0), so I holds again.  Overflow: A starts <= 0x4000 and gains <= 0x8000 within an
 // epoch, so it stays <= 0xC000 < 0x10000 and never carries into B.  With near-uniform bins a
 // sweep happens about once per 2^29 samples per CTA.
-constexpr uint32_t kSweepT = 0x4000;
-constexpr uint32_t kSweepMask = 0xC000C000u;   // bits >= 0x4000 of both halves
-constexpr uint32_t kSweepEpochIncs = 0x8000;   // per-epoch increment bound per CTA
+// (General form: with at most I increments per epoch, T = the largest power of two with
+// T + I <= 0xFFFF and the vote mask = the bits >= T of both halves.  I = 0x8000 gives the
+// T = 0x4000, mask 0xC000C000 above.)
+__host__ __device__ constexpr uint32_t sweep_threshold(uint32_t incs, uint32_t t = 0x8000) {
+  return (t + incs <= 0xFFFFu || t <= 1) ? t : sweep_threshold(incs, t >> 1);
+}
+__host__ __device__ constexpr uint32_t sweep_mask(uint32_t t) {
+  return ((0x10000u - t) & 0xFFFFu) * 0x10001u;
+}
+static_assert(sweep_threshold(0x8000) == 0x4000 && sweep_mask(0x4000) == 0xC000C000u, "sweep constants");
 
 // Bin (v >> 16) += 1 (or += 0 for a masked lane); returns the old word for the vote.  The
 // increment is a predicate test + SEL; the single-LOP3 form `(v & 0x10000) | one` (one = 1 in
