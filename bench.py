@@ -339,9 +339,11 @@ def roofline_for(w: SI.Workload, res, peaks, peaks_src, prof):
         mhz = peaks.get("sm_max_mhz", 1965.0)
         peak = 64.0 / 9.0 * SM_PER_GPU * mhz * 1e6 / 1e9
         achieved = res["samples_rank"] / (ms_launch * 1e-3) / 1e9
-        return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gsamples/s",
-                "frac": achieved / peak, "traffic": None,
-                "peak_note": "FMA-pipe floor 9 slots/sample (3 IMAD.WIDE x2 + 3 IMAD) at 64 slots/clk/SM, max SM clock"}
+        out = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gsamples/s",
+               "frac": achieved / peak, "traffic": None,
+               "peak_note": "FMA-pipe floor 9 slots/sample (3 IMAD.WIDE x2 + 3 IMAD) at 64 slots/clk/SM, max SM clock"}
+        out.update(_pipes(prof, w.name, "fused_kernel"))
+        return out
     bytes_launch = res["samples_rank"] * w.elem_bytes
     achieved = bytes_launch / (ms_launch * 1e-3) / 1e9
     peak = float(peaks["hbm_gbs"])
@@ -349,9 +351,22 @@ def roofline_for(w: SI.Workload, res, peaks, peaks_src, prof):
     kname = {"u32": "fill_kernel<0>", "u64": "fill_kernel<1>", "f32": "fill_kernel<2>"}[w.kind]
     if prof.get(w.name, {}).get("kernel") == kname and w.name in prof:
         traffic = prof[w.name].get("dram_bytes_per_launch")
-    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks_src}, copy read+write)",
-            "algorithmic_bytes_per_launch": bytes_launch}
+    out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+           "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks_src}, copy read+write)",
+           "algorithmic_bytes_per_launch": bytes_launch}
+    out.update(_pipes(prof, w.name, kname))
+    return out
+
+
+def _pipes(prof, name, kname):
+    """Pipe utilisation of the same kernel from the committed ncu capture (profiles/): what binds
+    when the HBM fraction is below 1 (the u32/f32 fills are IMAD+ALU-bound)."""
+    p = prof.get(name, {})
+    if p.get("kernel") != kname:
+        return {}
+    return {"pipes_ncu": {"fmaheavy_pct": p.get("fmaheavy_pct"), "alu_pct": p.get("alu_pct"),
+                          "issue_pct": p.get("issue_active_pct"),
+                          "source": "profiles/ncu_summary.json (ncu --set full, same kernel)"}}
 
 
 def main():
