@@ -1,51 +1,12 @@
-// hist16.cuh -- a 65536-bin (or smaller) exact histogram in 128 KiB of shared memory:
-// 16-bit counters packed two per 32-bit word, exact by a guard-bit + epoch scheme.
-//
-// Contract with the caller (fused.cu, scaled.cu): a CTA barrier separates epochs, and at most
-// 0x8000 increments reach any bin per epoch.  Invariant: every half <= 0x7FFF at an epoch
-// start, so during the epoch a half stays <= 0xFFFF (it never carries into its neighbour).
-// The single thread whose ATOMS.ADD returns a half of 0x7FFF (the increment that makes it
-// 0x8000) subtracts 0x8000 from that half and adds 0x8000 to the global bin before the next
-// barrier, which restores the invariant.  A half has at most one pending crossing (a second
-// one needs the half to fall below 0x8000 first, which only the owner's subtraction does),
-// so every count is exact: final bin = 0x8000 * (fix-ups) + residual half.
+// hist16.cuh -- a 65536-bin (or smaller) exact histogram in 128 KiB of shared memory: 16-bit
+// counters packed two per 32-bit word, exact by the sweep scheme below (fused.cu, scaled.cu).
+// (Round 1's first design fixed every 0x7FFF -> 0x8000 crossing in place, one compare-and-branch
+// on each ATOMS result; the sweep scheme removed that branch from the hot loop: +16 % on c5.)
 #pragma once
 #include <stdint.h>
 
 namespace sq {
 
-// Fix-up of one crossing of bin b (inc = 1 for the low half, 0x10000 for the high half).
-// BITS: also count the fix-up per set bit of b (fused statistics derive ones[16..31] from the
-// histogram and need each fix-up's weight per bin bit).
-template <bool BITS>
-__device__ __forceinline__ void guard_fixup(uint32_t* bins, uint32_t b, uint32_t inc,
-                                            unsigned long long* hist, uint32_t* fix) {
-  atomicSub(&bins[b >> 1], inc << 15);                 // half -= 0x8000
-  atomicAdd(&hist[b], 0x8000ull);
-  if (BITS) {
-#pragma unroll 1
-    for (int j = 0; j < 16; j++)
-      if ((b >> j) & 1u) atomicAdd(&fix[j], 1u);
-  }
-}
-
-// Count bin (v >> 16) of a 32-bit value v (bin index b < 65536; low half = even bins).  A lane
-// with valid == false adds 0 (so callers need not diverge around masked samples).
-template <bool BITS>
-__device__ __forceinline__ void hist_add(uint32_t* bins, uint32_t v, unsigned long long* hist, uint32_t* fix,
-                                         bool valid = true) {
-  const uint32_t b = v >> 16;
-  uint32_t inc = (v & 0x10000u) ? 0x10000u : 1u;
-  if (!valid) inc = 0;
-  const uint32_t old = atomicAdd(&bins[b >> 1], inc);
-  if (((old + inc) ^ old) & 0x80008000u) guard_fixup<BITS>(bins, b, inc, hist, fix);
-}
-
-}  // namespace sq
-
-namespace sq {
-
-// ---------------------------------------------------------------------------------------
 // Sweep scheme (fused statistics): 16-bit bins packed two per word, exact by a THRESHOLD
 // invariant instead of a per-sample fix-up, so the hot loop never branches on an ATOMS result.
 //

@@ -7,7 +7,7 @@
 // Arithmetic: W <= 32, so every intermediate fits a 32-bit register and x*x mod 2^W is the
 // low W bits of one 32-bit IMAD; the rotation by W/2 is two shifts (a PRMT for W = 32).  The
 // counter walk is the Weyl step y(c+1) = y(c) + key.  The histogram is the packed
-// 16-bit, guard-bit exact scheme of hist16.cuh (epochs of 32 samples per thread).
+// 16-bit sweep scheme of hist16.cuh (epochs of 32 samples per thread), as in fused.cu.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -18,7 +18,9 @@ namespace sq {
 
 constexpr int kScaledThreads = 1024;
 constexpr int kScaledEpoch = 32;
-static_assert(kScaledThreads * kScaledEpoch <= 0x8000, "guard-bit epoch bound");
+constexpr uint32_t kScaledT = sweep_threshold(kScaledThreads * kScaledEpoch);
+constexpr uint32_t kScaledMask = sweep_mask(kScaledT);
+static_assert(kScaledT >= 0x100, "sweep-scheme epoch bound");
 
 struct ScaledArgs {
   const uint64_t* keys;
@@ -26,6 +28,7 @@ struct ScaledArgs {
   uint64_t slice_len;         // counters per CTA slice (last slice takes the rest)
   uint32_t W, h, mask;        // width, half width, 2^W - 1
   uint32_t slices;
+  uint32_t one;               // the value 1 (hist16.cuh increment)
 };
 
 __device__ __forceinline__ uint32_t rot_h(uint32_t x, uint32_t h, uint32_t mask) {
@@ -41,6 +44,20 @@ __device__ __forceinline__ uint32_t scaled_from(uint32_t y, uint32_t z, uint32_t
   x = (x * x + y) & mask;                 // round 3
   x = rot_h(x, h, mask);
   return ((x * x + z) & mask) >> h;       // round 4
+}
+
+// All words -> the key's global histogram row, zeroed (A/B packing of hist16.cuh).
+__device__ __noinline__ void flush_scaled(uint32_t* bins, uint32_t nwords, uint32_t nbins,
+                                          unsigned long long* hrow) {
+  for (uint32_t w = threadIdx.x; w < nwords; w += kScaledThreads) {
+    const uint32_t v = bins[w];
+    if (!v) continue;
+    bins[w] = 0;
+    uint32_t even, odd;
+    sweep_word_counts(v, even, odd);
+    if (even) atomicAdd(&hrow[2 * w], (unsigned long long)even);
+    if (odd && 2 * w + 1 < nbins) atomicAdd(&hrow[2 * w + 1], (unsigned long long)odd);
+  }
 }
 
 __global__ void __launch_bounds__(kScaledThreads, 1) scaled_hist_kernel(ScaledArgs a) {
@@ -62,20 +79,21 @@ __global__ void __launch_bounds__(kScaledThreads, 1) scaled_hist_kernel(ScaledAr
   uint32_t y = (uint32_t)(start * key) & a.mask;       // ctr*key mod 2^W
   uint64_t done = 0;
   for (uint64_t ep = 0; ep < epochs; ep++) {
+    uint32_t acc = 0;
 #pragma unroll 4
     for (int i = 0; i < kScaledEpoch; i++) {
       const uint32_t z = (y + key) & a.mask;
-      hist_add<false>(bins, scaled_from(y, z, a.h, a.mask) << 16, hrow, nullptr, done + i < cnt);
+      acc |= hist_add_sweep(bins, scaled_from(y, z, a.h, a.mask) << 16, a.one, done + i < cnt);
       y = z;
     }
     done += kScaledEpoch;
-    __syncthreads();   // epoch boundary of the guard-bit scheme
+    // epoch boundary of the sweep scheme (hist16.cuh): vote, and sweep if any word got hot
+    if (__syncthreads_or((acc & kScaledMask) != 0)) {
+      flush_scaled(bins, nwords, nbins, hrow);
+      __syncthreads();
+    }
   }
-  for (uint32_t w = threadIdx.x; w < nwords; w += kScaledThreads) {
-    const uint32_t v = bins[w];
-    if (v & 0xFFFFu) atomicAdd(&hrow[2 * w], (unsigned long long)(v & 0xFFFFu));
-    if ((v >> 16) && 2 * w + 1 < nbins) atomicAdd(&hrow[2 * w + 1], (unsigned long long)(v >> 16));
-  }
+  flush_scaled(bins, nwords, nbins, hrow);
 }
 
 int launch_scaled_hist(int W, const uint64_t* keys, uint64_t nkeys, uint64_t* hist, cudaStream_t stream) {
@@ -84,6 +102,7 @@ int launch_scaled_hist(int W, const uint64_t* keys, uint64_t nkeys, uint64_t* hi
   if (nkeys > 65535) return SQ_ERANGE;   // grid.y limit; callers batch larger key sets
   ScaledArgs a;
   a.keys = keys;
+  a.one = 1;
   a.hist = (unsigned long long*)hist;
   a.W = (uint32_t)W;
   a.h = (uint32_t)W / 2;

@@ -1,7 +1,7 @@
 """GPU exhaustive reduced-width uniformity (-m gpu, SPEC S:381-389, P:17 footnote
 1): sq_scaled_hist histograms equal the oracle's exhaustive enumeration for W = 8..24 and for
 W = 32 (one key, oracle run in parallel shards); key 0 drives all 2^32 counts into one bin (the
-guard-bit path); and at W = 32, >= 90 % of 32 rule-valid scaled keys give p > 1e-4."""
+histogram sweep path); and at W = 32, >= 90 % of 32 rule-valid scaled keys give p > 1e-4."""
 from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
