@@ -7,11 +7,12 @@
 //  * One CTA of 1024 threads per SM (persistent), each thread owning one contiguous counter
 //    range, walked with the multiply-free Weyl/finite-difference step (squares_device.cuh).
 //  * hist: a 65536-bin histogram held in shared memory as 16-bit counters packed two per
-//    32-bit word (128 KiB; 32-bit bins would need 256 KiB > 227 KiB).  Exact by the sweep
-//    scheme of hist16.cuh: a CTA barrier follows every 32 samples per thread (<= 0x8000
-//    increments per epoch); each ATOMS's old word is ORed into a per-thread flag word, and
-//    the CTA sweeps all bins to global memory at a barrier where some half was seen >= 0x4000,
-//    so every half stays <= 0xC000.  No per-sample branch on an ATOMS result.
+//    32-bit word (128 KiB; 32-bit bins would need 256 KiB > 227 KiB): word w holds
+//    A = count(2w) + count(2w+1) and B = count(2w+1).  Exact by the sweep scheme of
+//    hist16.cuh: a CTA barrier follows every 32 samples per thread (<= 0x8000 increments per
+//    epoch); each ATOMS's old word is ORed into a per-thread flag word, and the CTA sweeps all
+//    bins to global memory at a barrier where some A was seen >= 0x4000, so A stays <= 0xC000.
+//    No per-sample branch on an ATOMS result.
 //  * ones[16..31] are derived exactly from the histogram (bit j of u is bit j-16 of its bin):
 //    from the bins each sweep (and the final flush) moves to global memory.
 //  * ones[0..15]: bit-sliced carry-save counting.  Two samples' low halves are packed in one
@@ -19,6 +20,7 @@
 //    (one epoch) into a weight-16 word, which is ripple-added into 6 vertical counter planes,
 //    flushed to shared-memory totals every 63 epochs.  ~1.3 LOP3 per sample.
 //  * At exit: residual bins -> global hist (RED.ADD.64), CTA bit totals -> global ones.
+//  * Source order: generation runs one 8-sample batch ahead of its reduction (SQ_FUSED_PIPE).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
