@@ -19,13 +19,18 @@
 
 namespace sq {
 
+#ifndef SQ_FILL_LANE_BYTES
+#define SQ_FILL_LANE_BYTES 64
+#endif
 template <int KIND>
 struct FillTraits {
   // ES = element bytes; SPL = samples per lane per chunk (64 bytes per lane = two 256-bit
   // stores); J = 32 * SPL counters per warp chunk = 2^LOGJ.
   static constexpr int ES = kind_elem_bytes(KIND);
-  static constexpr int SPL = 64 / ES;
-  static constexpr int LOGJ = (SPL == 16) ? 9 : 8;
+  static constexpr int LB = SQ_FILL_LANE_BYTES;   // bytes per lane per chunk (64: two 256-bit stores)
+  static constexpr int W = LB / 4;                 // 32-bit words per lane per chunk
+  static constexpr int SPL = LB / ES;
+  static constexpr int LOGJ = 5 + (SPL == 32 ? 5 : SPL == 16 ? 4 : SPL == 8 ? 3 : 2);
 };
 
 __device__ __forceinline__ void st256(void* p, const uint32_t* v) {
@@ -69,8 +74,8 @@ __device__ __forceinline__ RowConst<SPL> row_const(uint64_t key, uint64_t stride
 #endif
 template <int KIND>
 __host__ __device__ constexpr int fill_form() { return SQ_FILL_FORM >= 0 ? SQ_FILL_FORM : (KIND == KIND_U32 ? 3 : 0); }
-template <int KIND, int FORM>
-__device__ __forceinline__ void put(uint32_t (&v)[16], int j, uint64_t y, uint64_t z, uint64_t u, uint32_t one) {
+template <int KIND, int FORM, int NW>
+__device__ __forceinline__ void put(uint32_t (&v)[NW], int j, uint64_t y, uint64_t z, uint64_t u, uint32_t one) {
   if (KIND == KIND_U32 || KIND == KIND_F32) {
 #ifdef SQ_FILL_MIX2
     const uint32_t o = (KIND == KIND_U32) ? squares32_mix<SQ_FILL_MIX2, SQ_FILL_MIX3, SQ_FILL_MIX4>(y, z, u, one) : squares32_from<FORM>(y, z, u, one);
@@ -104,7 +109,7 @@ __device__ __forceinline__ void put(uint32_t (&v)[16], int j, uint64_t y, uint64
 #define SQ_FILL_Y3 0
 #endif
 template <int KIND, int SPL, bool STRIDED, bool CHAIN2 = false>
-__device__ __forceinline__ void gen_lane(const State& s, const RowConst<SPL>& rc, uint32_t (&v)[16], uint32_t one) {
+__device__ __forceinline__ void gen_lane(const State& s, const RowConst<SPL>& rc, uint32_t (&v)[FillTraits<KIND>::W], uint32_t one) {
   uint64_t y = s.y, u = s.u, e = s.e;
 #if SQ_FILL_Y3
   // y + key as a 3-input add y + (key - one) + one with the opaque one: IMAD cannot express a
@@ -139,7 +144,7 @@ __global__ void __launch_bounds__(kFillThreads, KEYIMM ? kFillMinBlocksImm : kFi
   constexpr int SPL = FillTraits<KIND>::SPL;
   constexpr int LOGJ = FillTraits<KIND>::LOGJ;
   constexpr int J = 32 * SPL;            // counters per warp chunk
-  static_assert((1 << LOGJ) == J && SPL * ES == 64, "chunk geometry");
+  static_assert((1 << LOGJ) == J && SPL * ES == FillTraits<KIND>::LB, "chunk geometry");
 
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warps_per_cta = blockDim.x >> 5;
@@ -169,7 +174,7 @@ __global__ void __launch_bounds__(kFillThreads, KEYIMM ? kFillMinBlocksImm : kFi
     State s = STRIDED ? state_at_strided(a.ctr0 + i0 * a.stride, rc.key, rc.K)
                       : state_at(a.ctr0 + i0, rc.key);
     while (cc < cc_stop) {
-      uint32_t v[16];
+      uint32_t v[FillTraits<KIND>::W];
       if (cc >= full_lo && cc < full_hi) {
         // fast path: a run of full chunks, two 256-bit stores per lane each
         uint64_t nfull = (full_hi < cc_stop ? full_hi : cc_stop) - cc;
@@ -180,10 +185,10 @@ __global__ void __launch_bounds__(kFillThreads, KEYIMM ? kFillMinBlocksImm : kFi
           gen_lane<KIND, SPL, STRIDED, SQ_FILL_CHAIN2 && !KEYIMM>(s, rc, v, a.one);
 #ifdef SQ_FILL_NOSTORE   // experiment: generation without the output stream
 #pragma unroll
-          for (int j = 0; j < 16; j++) nostore_acc ^= v[j];
+          for (int j = 0; j < FillTraits<KIND>::W; j++) nostore_acc ^= v[j];
 #else
-          st256(p, v);
-          st256(p + 32, v + 8);
+#pragma unroll
+          for (int q = 0; q < FillTraits<KIND>::W / 8; q++) st256(p + 32 * q, v + 8 * q);
 #endif
           jump<LOGJ>(s, rc.jk, rc.cj, rc.dj);
           p += J * ES;
