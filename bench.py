@@ -329,6 +329,22 @@ def run_e2e(args, w, sq, key0, keys_d, ctr0, n, kn, dev, world):
             "note": "sq_fill_host / fused_stats + D2H of the counts; the 8-byte key travels in the launch parameters"}
 
 
+def config_for(w: SI.Workload, world: int, scaling: str) -> dict:
+    """The `config` object of the JSON line -- identical for both arms (ours and --impl reference)."""
+    per_rank = w.nkeys * w.n
+    return {"workload": f"{w.name}: " + {
+        "c2": "squares32 fill, 1 key (seed 1), ctr 0..2^30-1, uint32 out (4 GiB)",
+        "c3": "squares64 fill, 1 key (seed 1), ctr 0..2^29-1, uint64 out (4 GiB)",
+        "c4": "squares32->f32 fill, 4096 keys (seed 7) x 2^18 ctr, [key][ctr] (4 GiB)",
+        "c5": "fused squares32 hist(65536)+ones(32), 1 key (seed 1), ctr 0..2^38-1"}[w.name],
+        "key_seed": w.key_seed, "nkeys": w.nkeys, "ctr0": w.ctr0, "n_per_key": w.n,
+        "samples_per_step": per_rank * world if scaling == "weak" else per_rank,
+        "sharding": "counter" if w.shard == "ctr" else "key",
+        "parallelism": f"{'ctr' if w.shard == 'ctr' else 'key'}-shard x{world}",
+        "l2": "output larger than L2 (4 GiB written per step)" if w.kind != "fused"
+        else "no HBM traffic (fused, counts only)"}
+
+
 def roofline_for(w: SI.Workload, res, peaks, peaks_src, prof):
     """Roofline of the dominant (only) kernel of the step."""
     ms_launch = res["ms_per_step"]
@@ -436,17 +452,7 @@ def main():
             "scaling": args.scaling, "vs_baseline": None,
             "dtype": {"u32": "u32", "u64": "u64", "f32": "u32->f32", "fused": "u32"}[w.kind],
             "data": "synthetic",
-            "config": {"workload": f"{w.name}: " + {
-                "c2": "squares32 fill, 1 key (seed 1), ctr 0..2^30-1, uint32 out (4 GiB)",
-                "c3": "squares64 fill, 1 key (seed 1), ctr 0..2^29-1, uint64 out (4 GiB)",
-                "c4": "squares32->f32 fill, 4096 keys (seed 7) x 2^18 ctr, [key][ctr] (4 GiB)",
-                "c5": "fused squares32 hist(65536)+ones(32), 1 key (seed 1), ctr 0..2^38-1"}[w.name],
-                "key_seed": w.key_seed, "nkeys": w.nkeys, "ctr0": w.ctr0, "n_per_key": w.n,
-                "samples_per_step": res["samples_per_step"],
-                "sharding": "counter" if w.shard == "ctr" else "key",
-                "parallelism": f"{'ctr' if w.shard == 'ctr' else 'key'}-shard x{world}",
-                "l2": "output larger than L2 (4 GiB written per step)" if w.kind != "fused"
-                else "no HBM traffic (fused, counts only)"},
+            "config": config_for(w, world, args.scaling),
             "roofline": rl,
             "cpu_baseline": {"value": rate / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{samples} samples of {w.name}: {shape}; {wall:.2f} s wall"},
@@ -489,10 +495,10 @@ def main_reference(args, w, rank, world):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": {"u32": "u32", "u64": "u64", "f32": "u32->f32",
-                                                           "fused": "u32"}[w.kind],
+        "scaling": args.scaling, "vs_baseline": None, "dtype": {"u32": "u32", "u64": "u64", "f32": "u32->f32",
+                                                               "fused": "u32"}[w.kind],
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": w.name, "key_seed": w.key_seed, "nkeys": w.nkeys, "n_per_key": w.n},
+        "config": config_for(w, world, args.scaling),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": f"per step {last[0]} samples: {last[1]}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
