@@ -371,6 +371,10 @@ def roofline_for(w: SI.Workload, res, peaks, peaks_src, prof):
            "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks_src}, copy read+write)",
            "algorithmic_bytes_per_launch": bytes_launch}
     out.update(_pipes(prof, w.name, kname))
+    # the same achieved rate against the other write ceilings SURVEY.md 8(d) names (context only)
+    out["other_peaks"] = {"spec_8000_GBps": achieved / 8000.0,
+                          "memset_7354_GBps (profiles/r01_microbench_writes.json)": achieved / 7354.4,
+                          "sm_store_6327_GBps (STG.256, same file)": achieved / 6326.5}
     return out
 
 
