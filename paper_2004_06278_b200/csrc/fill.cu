@@ -72,6 +72,9 @@ __device__ __forceinline__ RowConst<SPL> row_const(uint64_t key, uint64_t stride
 #ifndef SQ_FILL_FORM
 #define SQ_FILL_FORM -1
 #endif
+#ifndef SQ_FILL_FMUL2
+#define SQ_FILL_FMUL2 1   // f32 scale as a packed FMUL2 over word pairs (gen_lane)
+#endif
 template <int KIND>
 __host__ __device__ constexpr int fill_form() { return SQ_FILL_FORM >= 0 ? SQ_FILL_FORM : (KIND == KIND_U32 ? 3 : 0); }
 template <int KIND, int FORM, int NW>
@@ -82,7 +85,11 @@ __device__ __forceinline__ void put(uint32_t (&v)[NW], int j, uint64_t y, uint64
 #else
     const uint32_t o = squares32_from<FORM>(y, z, u, one);
 #endif
-    v[j] = (KIND == KIND_F32) ? __float_as_uint(u32_to_unit_f32(o)) : o;
+    // f32: the exact integer float(u >> 8) here; the 2^-24 scale is applied to pairs of lanes'
+    // words afterwards with one packed FMUL2 (scale_f32_pairs), exact as before
+    v[j] = (KIND == KIND_F32) ? (SQ_FILL_FMUL2 ? __float_as_uint(__uint2float_rn(o >> 8))
+                                               : __float_as_uint(u32_to_unit_f32(o)))
+                              : o;
   } else {
     const uint64_t o = squares64_from<FORM>(y, z, u, one);
     if (KIND == KIND_U64) {
@@ -96,6 +103,19 @@ __device__ __forceinline__ void put(uint32_t (&v)[NW], int j, uint64_t y, uint64
       v[2 * j] = __float_as_uint(u32_to_unit_f32(lo32(o)));
       v[2 * j + 1] = __float_as_uint(u32_to_unit_f32(hi32(o)));
     }
+  }
+}
+
+// (float)(u >> 8) * 2^-24 for two words at once: one FMUL2 (packed f32x2 multiply, sm_100) by
+// the exact power of two -- same bits as u32_to_unit_f32 (BASELINE.json config 4).
+template <int NW>
+__device__ __forceinline__ void scale_f32_pairs(uint32_t (&v)[NW]) {
+#pragma unroll
+  for (int i = 0; i < NW; i += 2) {
+    unsigned long long x = ((unsigned long long)v[i + 1] << 32) | v[i], r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(0x3380000033800000ull));
+    v[i] = (uint32_t)r;
+    v[i + 1] = (uint32_t)(r >> 32);
   }
 }
 
@@ -134,6 +154,7 @@ __device__ __forceinline__ void gen_lane(const State& s, const RowConst<SPL>& rc
       }
     }
   }
+  if (KIND == KIND_F32 && SQ_FILL_FMUL2) scale_f32_pairs(v);
 }
 
 // KEYIMM: a single row whose key is a kernel parameter, so ptxas can keep the key and the
