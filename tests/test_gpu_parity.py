@@ -151,6 +151,30 @@ def test_fill_full_size_single_key(sq, cfg):
     assert np.array_equal(got, want), first_mismatch(got, want)
 
 
+@pytest.mark.parametrize("kind", ["u32", "u64"])
+def test_fill_beyond_2_32_elements(sq, kind):
+    """Maximum-size edge: one row of 2^32 + 1000 elements (16/32 GiB) starting 2^31 counters
+    before the 2^64 wrap, through the key-by-value entry point bench.py times.  Every element
+    index and byte offset passes 2^32; checked against the oracle's pair evaluator on the first
+    and last 2^20 elements, 2^20 random ones and the elements around the wrap."""
+    key = int(O.keygen(1, 1)[0])
+    n = (1 << 32) + 1000
+    ctr0 = (1 << 64) - (1 << 31)
+    es = 8 if kind == "u64" else 4
+    out = torch.empty(n, dtype=torch.int32 if es == 4 else torch.int64, device="cuda")
+    getattr(sq, f"fill_{kind}_k")(key, ctr0, n, out=out)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(20040627)
+    idx = np.unique(np.concatenate([np.arange(1 << 20), np.arange(n - (1 << 20), n),
+                                    rng.integers(0, n, 1 << 20), np.arange((1 << 31) - 8, (1 << 31) + 8)]))
+    got = out[torch.from_numpy(idx).cuda()].cpu().numpy().view(np.uint32 if es == 4 else np.uint64)
+    ctr = (np.uint64(ctr0) + idx.astype(np.uint64))   # wraps mod 2^64 in uint64 arithmetic
+    want = O.squares_pairs(ctr, np.full(idx.shape, key, dtype=np.uint64), width=32 if es == 4 else 64)
+    assert np.array_equal(got, want), first_mismatch(got, want)
+    del out
+    torch.cuda.empty_cache()
+
+
 def test_fill_full_size_c4(sq):
     """BASELINE.json config 4: 4096 keys (seed 7) x 2^18 counters as float32, [key][ctr]."""
     w = SI.CONFIGS["c4"]
