@@ -45,7 +45,7 @@ constexpr int kPlanes = 6;                        // vertical planes for weight-
 constexpr int kFlushEvery = 63 / kTrees;          // epochs between plane flushes
 static_assert(kEpoch % 32 == 0 && kTrees >= 1, "fused geometry");
 static_assert(kT >= 0x100 && kT + kEpochIncs <= 0xFFFFu, "epoch bound of the sweep scheme");
-constexpr size_t kFusedSmem = 32768 * 4 + 16 * 8 + 16 * 8;
+constexpr size_t kFusedSmem = 32768 * 4 + 16 * 8 + 16 * 8 + 2 * 4;
 
 // carry-save adder: (h, l) = (maj(a,b,c), a^b^c)
 __device__ __forceinline__ void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32_t b, uint32_t c) {
@@ -204,9 +204,11 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
   uint32_t* bins = smem;
   unsigned long long* lo_cnt = (unsigned long long*)(smem + 32768);
   unsigned long long* hi_cnt = lo_cnt + 16;
+  volatile uint32_t* hot_stamp = (volatile uint32_t*)(hi_cnt + 16);   // [2], epoch-stamped vote
   const uint32_t tid = threadIdx.x;
   for (uint32_t i = tid; i < 32768; i += kFusedThreads) bins[i] = 0;
   if (tid < 16) { lo_cnt[tid] = 0; hi_cnt[tid] = 0; }
+  if (tid < 2) hot_stamp[tid] = 0;
   __syncthreads();
 
   const uint64_t t = (uint64_t)blockIdx.x * kFusedThreads + tid;
@@ -262,8 +264,14 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
       for (int p = 0; p < kPlanes; p++) { columns_add(colcnt, pl[p], 16u << p); pl[p] = 0; }
       warp_flush16(colcnt, lo_cnt);
     }
-    // epoch boundary of the sweep scheme (hist16.cuh): vote, and sweep if any half got hot
-    if (__syncthreads_or((acc & kMask) != 0)) {
+    // epoch boundary of the sweep scheme (hist16.cuh): vote, and sweep if any word got hot.
+    // The vote is an epoch-stamped flag + a plain barrier (BAR.SYNC) instead of the reduction
+    // barrier __syncthreads_or (BAR.RED.OR): +0.9 % here, +4 % in scaled.cu.  Stamps are unique per
+    // epoch, so the flag is never reset; two slots keep epoch e+1's writers off epoch e's slot
+    // until every thread has read it (they only write after the next barrier).
+    if (acc & kMask) hot_stamp[ep & 1] = ep + 1;
+    __syncthreads();
+    if (hot_stamp[ep & 1] == ep + 1) {
       flush_bins(bins, hist, hi_cnt);
       __syncthreads();
     }

@@ -63,6 +63,9 @@ __device__ __noinline__ void flush_scaled(uint32_t* bins, uint32_t nwords, uint3
 __global__ void __launch_bounds__(kScaledThreads, 1) scaled_hist_kernel(ScaledArgs a) {
   extern __shared__ __align__(16) uint32_t bins[];
   const uint32_t nbins = 1u << a.h, nwords = (nbins + 1) / 2;
+  __shared__ uint32_t hot_stamp_[2];
+  volatile uint32_t* hot_stamp = hot_stamp_;
+  if (threadIdx.x < 2) hot_stamp[threadIdx.x] = 0;
   for (uint32_t i = threadIdx.x; i < nwords; i += kScaledThreads) bins[i] = 0;
   __syncthreads();
   const uint64_t krow = blockIdx.y;
@@ -87,8 +90,11 @@ __global__ void __launch_bounds__(kScaledThreads, 1) scaled_hist_kernel(ScaledAr
       y = z;
     }
     done += kScaledEpoch;
-    // epoch boundary of the sweep scheme (hist16.cuh): vote, and sweep if any word got hot
-    if (__syncthreads_or((acc & kScaledMask) != 0)) {
+    // epoch boundary of the sweep scheme (hist16.cuh): epoch-stamped vote + plain barrier
+    // (as fused.cu), sweep if any word got hot
+    if (acc & kScaledMask) hot_stamp[ep & 1] = (uint32_t)ep + 1;
+    __syncthreads();
+    if (hot_stamp[ep & 1] == (uint32_t)ep + 1) {
       flush_scaled(bins, nwords, nbins, hrow);
       __syncthreads();
     }
