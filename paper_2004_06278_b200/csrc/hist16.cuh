@@ -18,7 +18,8 @@ namespace sq {
 // Contract: a CTA barrier separates epochs and at most 0x8000 increments reach any word per
 // epoch.  Invariant I: A <= T = 0x4000 in every word at an epoch start (B <= A).
 // Each thread ORs the OLD word returned by each of its ATOMS into `acc`; at the epoch barrier
-// the CTA votes (__syncthreads_or) on (acc & 0xC000C000) -- "some A (or B) was seen at >= 0x4000
+// the CTA votes on (acc & 0xC000C000) (an epoch-stamped shared flag + a plain barrier, see
+// fused.cu) -- "some A (or B) was seen at >= 0x4000
 // before an increment".  No vote => every increment found A < 0x4000, so every A ends the epoch
 // <= 0x4000 and I holds.  A vote => the CTA sweeps all bins to the global histogram (every
 // word -> 0), so I holds again.  Overflow: A starts <= 0x4000 and gains <= 0x8000 within an
