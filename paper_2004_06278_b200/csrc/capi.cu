@@ -18,14 +18,14 @@ int set_cuda_error(cudaError_t e) {
 }
 
 static std::mutex g_dev_mu;
-static DeviceInfo g_dev[64];
-static bool g_dev_ok[64];
+static DeviceInfo g_dev[kMaxDevices];
+static bool g_dev_ok[kMaxDevices];
 
 const DeviceInfo* device_info() {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) { set_cuda_error(e); return nullptr; }
-  if (dev < 0 || dev >= 64) { set_cuda_error(cudaErrorInvalidDevice); return nullptr; }
+  if (dev < 0 || dev >= kMaxDevices) { set_cuda_error(cudaErrorInvalidDevice); return nullptr; }
   std::lock_guard<std::mutex> lk(g_dev_mu);
   if (!g_dev_ok[dev]) {
     DeviceInfo d;

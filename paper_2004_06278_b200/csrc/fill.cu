@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "squares_device.cuh"
 #include "sq_internal.h"
 
@@ -258,9 +260,17 @@ static int launch_fill(const FillArgs& a0, uint64_t nkeys, uint64_t n, cudaStrea
   void (*kern)(FillArgs);
   if (a.stride == 1) kern = a.keys ? fill_kernel<KIND, false, false> : fill_kernel<KIND, true, false>;
   else kern = a.keys ? fill_kernel<KIND, false, true> : fill_kernel<KIND, true, true>;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFillThreads, 0);
-  if (e != cudaSuccess) return set_cuda_error(e);
-  if (occ < 1) occ = 1;
+  // occupancy is a property of (device, kernel): queried once, then cached (host overhead per
+  // call matters in the launch-bound small-n regime)
+  static std::atomic<int> occ_cache[kMaxDevices][2][2];
+  std::atomic<int>& oc = occ_cache[di->device][a.keys ? 0 : 1][a.stride == 1 ? 0 : 1];
+  occ = oc.load(std::memory_order_relaxed);
+  if (occ == 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFillThreads, 0);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    if (occ < 1) occ = 1;
+    oc.store(occ, std::memory_order_relaxed);
+  }
   uint64_t blocks = (uint64_t)di->sms * occ;
   const uint64_t wpc = kFillThreads / 32;
   // no more warps than chunks

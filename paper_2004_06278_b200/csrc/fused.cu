@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "hist16.cuh"
 #include "squares_device.cuh"
 #include "sq_internal.h"
@@ -303,8 +305,14 @@ int launch_fused(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint3
   decltype(&fused_kernel<false, false>) kern =
       strided ? (bitrev ? fused_kernel<true, true> : fused_kernel<true, false>)
               : (bitrev ? fused_kernel<false, true> : fused_kernel<false, false>);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFusedSmem);
-  if (e != cudaSuccess) return set_cuda_error(e);
+  // the 128 KiB opt-in is a per-(device, kernel) attribute: set once, then cached
+  static std::atomic<bool> attr_set[kMaxDevices][4];
+  std::atomic<bool>& as = attr_set[di->device][(strided ? 2 : 0) + (bitrev ? 1 : 0)];
+  if (!as.load(std::memory_order_acquire)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFusedSmem);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    as.store(true, std::memory_order_release);
+  }
   // one CTA per SM; small n uses fewer CTAs (>= 2^20 samples each) so the flush amortises
   uint64_t blocks = (n + (1ull << 20) - 1) >> 20;
   if (blocks > (uint64_t)di->sms) blocks = di->sms;

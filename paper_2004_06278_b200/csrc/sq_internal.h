@@ -44,6 +44,8 @@ struct FillArgs {
   uint32_t one;             // always 1: the opaque shift amount of squares_dev.cuh cross_add
 };
 
+constexpr int kMaxDevices = 64;   // per-device caches (device_info, occupancy, attributes)
+
 struct DeviceInfo {
   int device;
   int sms;
