@@ -40,3 +40,19 @@ extern "C" int devapi_stream(uint64_t key, uint64_t ctr0, uint64_t per, uint64_t
   k_stream<<<(unsigned)((threads + 127) / 128), 128>>>(key, ctr0, per, skip0, kind, threads, out);
   return (int)cudaDeviceSynchronize();
 }
+
+// Generate-inside-the-consumer throughput (tools/bench_next.py): thread t draws `per`
+// consecutive squares32 values of Stream(ctr0 + t*per, key) and XOR-folds them (nothing
+// stored but one word per thread).  Asynchronous on the default stream (timed with events).
+__global__ void k_stream_xor(uint64_t key, uint64_t ctr0, uint64_t per, uint32_t* out) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  sq::Stream st(ctr0 + t * per, key);
+  uint32_t acc = 0;
+  for (uint64_t i = 0; i < per; i++) acc ^= st.next_u32();
+  out[t] = acc;
+}
+
+extern "C" int devapi_stream_xor(uint64_t key, uint64_t ctr0, uint64_t per, uint64_t blocks, uint32_t* out) {
+  k_stream_xor<<<(unsigned)blocks, 256>>>(key, ctr0, per, out);
+  return (int)cudaGetLastError();
+}

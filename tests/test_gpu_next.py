@@ -80,6 +80,30 @@ def test_keyctr(sq, kind, ctr):
     assert np.array_equal(got, want), first_mismatch(got, want)
 
 
+@pytest.mark.parametrize("kind", ["u32", "u64", "f32", "f64", "f32x2"])
+@pytest.mark.parametrize("nkeys,koff,ooff", [(1, 0, 0), (3, 0, 0), (4, 0, 0), (4097, 1, 0), (4098, 0, 1), (70_001, 1, 1)])
+def test_keyctr_alignment_and_tails(sq, kind, nkeys, koff, ooff):
+    """Key-counter mode's vectorised path (4 keys per thread, 16-byte loads/stores) and its
+    per-key fallback: ragged key counts, keys and outputs offset by one element (unaligned)."""
+    keys = O.keygen(12, nkeys)
+    kbuf = torch.zeros(nkeys + 1, dtype=torch.int64, device="cuda")
+    kbuf[koff:koff + nkeys] = _dev_keys(keys)
+    es = 8 if kind in ("u64", "f64", "f32x2") else 4
+    obuf = torch.full((nkeys + 2,), -1, dtype=torch.int64 if es == 8 else torch.int32, device="cuda")
+    dt = {"u32": torch.int32, "u64": torch.int64, "f32": torch.float32, "f64": torch.float64, "f32x2": torch.float32}[kind]
+    view = obuf[ooff:ooff + nkeys].view(dt)
+    if kind == "f32x2":
+        view = view.view(nkeys, 2)
+    sq.fill_keyctr(kind, kbuf[koff:koff + nkeys], 4242, out=view)
+    torch.cuda.synchronize()
+    want = O.fill_keyctr(kind, keys, 4242)
+    allb = obuf.cpu().numpy().view(np.uint64 if es == 8 else np.uint32)
+    got = allb[ooff:ooff + nkeys]
+    assert np.array_equal(got, want.reshape(-1).view(got.dtype)[:nkeys]), first_mismatch(got, want)
+    assert (allb[:ooff] == allb.dtype.type(-1 & (2 ** (8 * es) - 1))).all()
+    assert (allb[ooff + nkeys:] == allb.dtype.type(-1 & (2 ** (8 * es) - 1))).all()
+
+
 @pytest.mark.parametrize("stride,bitrev", [(1, True), (2, False), (3, True), (1 << 40, False)])
 @pytest.mark.parametrize("n", [1000, (1 << 22) + 7])
 def test_fused_ex(sq, stride, bitrev, n):
