@@ -35,15 +35,27 @@ __device__ __forceinline__ uint32_t rot_h(uint32_t x, uint32_t h, uint32_t mask)
   return ((x >> h) | (x << h)) & mask;
 }
 
-// squares32_scaled for one counter given y = ctr*key and z = y + key (both mod 2^W).
+// squares32_scaled for one counter given y = ctr*key and z = y + key (both mod 2^W), returned
+// in histogram position: the W/2-bit output v shifted to bits 16.. (v << 16 for W < 32; for
+// W = 32 the round-4 sum itself, whose bits 16..31 ARE v: hist16.cuh reads only those).
+// W32: mask = all ones (no AND) and the rotation by 16 is one funnel shift.
+template <bool W32>
 __device__ __forceinline__ uint32_t scaled_from(uint32_t y, uint32_t z, uint32_t h, uint32_t mask) {
+  if (W32) {
+    uint32_t x = __funnelshift_l(y * y + y, y * y + y, 16);   // round 1 + rotation
+    x = x * x + z;                                            // round 2
+    x = __funnelshift_l(x, x, 16);
+    x = x * x + y;                                            // round 3
+    x = __funnelshift_l(x, x, 16);
+    return x * x + z;                                         // round 4 (bits 16..31 = output)
+  }
   uint32_t x = (y * y + y) & mask;        // round 1
   x = rot_h(x, h, mask);
   x = (x * x + z) & mask;                 // round 2
   x = rot_h(x, h, mask);
   x = (x * x + y) & mask;                 // round 3
   x = rot_h(x, h, mask);
-  return ((x * x + z) & mask) >> h;       // round 4
+  return (((x * x + z) & mask) >> h) << 16;   // round 4
 }
 
 // All words -> the key's global histogram row, zeroed (A/B packing of hist16.cuh).
@@ -60,6 +72,7 @@ __device__ __noinline__ void flush_scaled(uint32_t* bins, uint32_t nwords, uint3
   }
 }
 
+template <bool W32>
 __global__ void __launch_bounds__(kScaledThreads, 1) scaled_hist_kernel(ScaledArgs a) {
   extern __shared__ __align__(16) uint32_t bins[];
   const uint32_t nbins = 1u << a.h, nwords = (nbins + 1) / 2;
@@ -83,11 +96,20 @@ __global__ void __launch_bounds__(kScaledThreads, 1) scaled_hist_kernel(ScaledAr
   uint64_t done = 0;
   for (uint64_t ep = 0; ep < epochs; ep++) {
     uint32_t acc = 0;
+    if (done + kScaledEpoch <= cnt) {
+#pragma unroll 8
+      for (int i = 0; i < kScaledEpoch; i++) {
+        const uint32_t z = W32 ? y + key : (y + key) & a.mask;
+        acc |= hist_add_sweep(bins, scaled_from<W32>(y, z, a.h, a.mask), a.one);
+        y = z;
+      }
+    } else {
 #pragma unroll 4
-    for (int i = 0; i < kScaledEpoch; i++) {
-      const uint32_t z = (y + key) & a.mask;
-      acc |= hist_add_sweep(bins, scaled_from(y, z, a.h, a.mask) << 16, a.one, done + i < cnt);
-      y = z;
+      for (int i = 0; i < kScaledEpoch; i++) {
+        const uint32_t z = W32 ? y + key : (y + key) & a.mask;
+        acc |= hist_add_sweep(bins, scaled_from<W32>(y, z, a.h, a.mask), a.one, done + i < cnt);
+        y = z;
+      }
     }
     done += kScaledEpoch;
     // epoch boundary of the sweep scheme (hist16.cuh): epoch-stamped vote + plain barrier
@@ -122,9 +144,10 @@ int launch_scaled_hist(int W, const uint64_t* keys, uint64_t nkeys, uint64_t* hi
   a.slices = (uint32_t)slices;
   a.slice_len = total / slices;
   const size_t smem = (size_t)(((1u << a.h) + 1) / 2) * 4;
-  cudaError_t e = cudaFuncSetAttribute(scaled_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = (W == 32) ? scaled_hist_kernel<true> : scaled_hist_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return set_cuda_error(e);
-  scaled_hist_kernel<<<dim3((unsigned)slices, (unsigned)nkeys), kScaledThreads, smem, stream>>>(a);
+  kern<<<dim3((unsigned)slices, (unsigned)nkeys), kScaledThreads, smem, stream>>>(a);
   return set_cuda_error(cudaGetLastError());
 }
 
