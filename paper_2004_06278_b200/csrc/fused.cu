@@ -334,39 +334,69 @@ int launch_fused(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint3
 // SURVEY.md 8(f)3).  The stream is the outputs u_0, u_1, ... of counters
 // ctr0 + i*stride, each read least-significant bit first; transitions = #{adjacent bit pairs
 // that differ} = sum_i popc((u_i ^ (u_i >> 1)) & 0x7FFFFFFF) + sum_{i>0} (bit31(u_{i-1}) != bit0(u_i)).
-// Each thread walks one contiguous index range and also evaluates the sample before it (one
+// Each thread walks one contiguous index range and also evaluates the sample after it (one
 // extra sample per thread) for the boundary pair.  Accumulates into *count.
 namespace sq {
 
 template <bool STRIDED, bool BITREV>
 __global__ void __launch_bounds__(256)
 transitions_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint64_t q, uint64_t r,
-                   unsigned long long* __restrict__ count) {
+                   unsigned long long* __restrict__ count, uint32_t one) {
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t start = t * q + (t < r ? t : r);
   const uint64_t cnt = q + (t < r ? 1 : 0);
   const uint64_t K = STRIDED ? stride * key : key;
   uint64_t acc = 0;
   if (cnt) {
+    // Each sample u_i contributes popc(u_i ^ funnel(u_i, u_{i+1})): bits 0..30 are its own 31
+    // adjacent pairs, bit 31 is the pair (bit31(u_i), bit0(u_{i+1})) across the boundary.  The
+    // thread's last sample pairs with the next thread's first (evaluated directly), or with
+    // nothing at the end of the stream.  Full 8-sample batches come from gen8 (the fused
+    // kernel's walk); the < 8 remaining samples from the per-counter step.
     State s = STRIDED ? state_at_strided(ctr0 + start * stride, key, K) : state_at(ctr0 + start, key);
-    const uint64_t k2x2 = 2 * K * K;
-    uint32_t prev_bit31 = 0;
-    if (start > 0) {   // boundary with the previous thread's last sample
-      const uint64_t cp = STRIDED ? ctr0 + (start - 1) * stride : ctr0 + (start - 1);
-      uint32_t up = squares32(cp, key);
-      if (BITREV) up = __brev(up);
-      prev_bit31 = up >> 31;
+    WalkConst wc;
+    {
+      const uint64_t k2x2 = 2 * K * K;
+      wc.key = key;
+      wc.K = K;
+      wc.cst[0] = 0;
+#pragma unroll
+      for (int j = 1; j < 8; j++) wc.cst[j] = wc.cst[j - 1] + k2x2;
+      wc.cst8 = wc.cst[7] + k2x2;
     }
-    for (uint64_t i = 0; i < cnt; i++) {
+    uint32_t prev = 0, part = 0;
+    bool have = false;
+    uint64_t i = 0;
+    for (; i + 8 <= cnt; i += 8) {
+      uint32_t v[8];
+      gen8<STRIDED, BITREV>(s, wc, v, one);
+      uint32_t bp = have ? __popc(prev ^ __funnelshift_r(prev, v[0], 1)) : 0u;   // <= 256 per batch
+#pragma unroll
+      for (int j = 0; j < 7; j++) bp += __popc(v[j] ^ __funnelshift_r(v[j], v[j + 1], 1));
+      acc += bp;
+      prev = v[7];
+      have = true;
+    }
+    const uint64_t k2x2 = 2 * K * K;
+    for (; i < cnt; i++) {
       const uint64_t z = add64(s.y, key);
       uint32_t u = squares32_from(s.y, z, s.u);
       if (BITREV) u = __brev(u);
-      acc += __popc((u ^ (u >> 1)) & 0x7FFFFFFFu);
-      if (start + i > 0) acc += (prev_bit31 ^ u) & 1u;
-      prev_bit31 = u >> 31;
+      if (have) part += __popc(prev ^ __funnelshift_r(prev, u, 1));
+      prev = u;
+      have = true;
       if (STRIDED) s.y = add64(s.y, K); else s.y = z;
       s.u = add64(s.u, s.e);
       s.e = add64(s.e, k2x2);
+    }
+    acc += part;
+    if (start + cnt < n) {   // boundary with the next thread's first sample
+      const uint64_t cn = STRIDED ? ctr0 + (start + cnt) * stride : ctr0 + (start + cnt);
+      uint32_t un = squares32(cn, key);
+      if (BITREV) un = __brev(un);
+      acc += __popc(prev ^ __funnelshift_r(prev, un, 1));
+    } else {
+      acc += __popc((prev ^ (prev >> 1)) & 0x7FFFFFFFu);
     }
   }
   // warp reduction (64-bit), one atomic per warp
@@ -387,7 +417,7 @@ int launch_transitions(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n,
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   const uint64_t T = blocks * 256;
-  kern<<<(unsigned)blocks, 256, 0, stream>>>(key, ctr0, stride, n, n / T, n % T, (unsigned long long*)count);
+  kern<<<(unsigned)blocks, 256, 0, stream>>>(key, ctr0, stride, n, n / T, n % T, (unsigned long long*)count, 1u);
   return set_cuda_error(cudaGetLastError());
 }
 

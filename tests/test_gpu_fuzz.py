@@ -9,6 +9,7 @@ import pytest
 import torch
 
 import oracle as O
+import oracle.battery as OB
 
 pytestmark = pytest.mark.gpu
 M64 = (1 << 64) - 1
@@ -91,3 +92,21 @@ def test_fused_fuzz(sq, i):
     hw, ow = O.fused_stats_ex(key, ctr0, stride, n, bitrev)
     assert np.array_equal((h - h0).cpu().numpy().view(np.uint64), hw), (i, ctr0, n, stride, bitrev, key)
     assert np.array_equal((o - o0).cpu().numpy().view(np.uint64), ow), (i, ctr0, n, stride, bitrev, key)
+
+
+@pytest.mark.parametrize("i", range(16))
+def test_transitions_fuzz(sq, i):
+    """sq_transitions (runs statistic) on ragged lengths (n < 8, n % 8 != 0: the scalar tail and
+    the per-thread boundary pairs), strides, bit reversal, accumulation onto a non-zero count;
+    against the oracle stream's direct bit comparison."""
+    rng, ctr0, n, stride = _case(i, 3)
+    n = _pick(rng, [1, 2, 7, 8, 9, 255, 4103, int(rng.integers(1, 300_000))])
+    bitrev = bool(rng.random() < 0.5)
+    key = int(O.keygen(int(rng.integers(0, 1 << 31)), 1)[0])
+    c = torch.full((1,), 1 << 40, dtype=torch.int64, device="cuda")
+    sq.transitions(key, ctr0, n, stride=stride, bitrev=bitrev, count=c)
+    torch.cuda.synchronize()
+    w = O.fill_strided("u32", [key], ctr0, stride, n)[0]
+    if bitrev:
+        w = np.array([O.bitrev32(int(x)) for x in w], np.uint32)
+    assert int(c.item()) - (1 << 40) == OB.counts(w)["transitions"], (i, ctr0, n, stride, bitrev)
