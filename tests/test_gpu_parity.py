@@ -298,3 +298,22 @@ def test_fill_host_e2e(sq):
         got = host.numpy().view(VIEW[kind])
         want = O.fill(kind, [key], 99, n)[0].view(VIEW[kind])
         assert np.array_equal(got, want), (kind, first_mismatch(got, want))
+
+
+@pytest.mark.parametrize("kind", ["u32", "u64", "f32", "f64", "f32x2"])
+@pytest.mark.parametrize("scratch_bytes,n,ctr0", [(64, 1000, 5), (100, 4097, (1 << 64) - 700), (3 << 20, (1 << 21) + 9, 1 << 40)])
+def test_fill_host_chunking(sq, kind, scratch_bytes, n, ctr0):
+    """sq_fill_host with tiny and odd scratch sizes (chunks of one or a few 32-byte halves, ragged
+    last chunk, the counter wrap inside the range) and pageable as well as pinned host memory."""
+    key = int(O.keygen(2, 1)[0])
+    es = 8 if kind in ("u64", "f64", "f32x2") else 4
+    for pinned in (True, False):
+        host = torch.zeros(n * es + 16, dtype=torch.uint8)
+        if pinned:
+            host = host.pin_memory()
+        scratch = torch.empty(scratch_bytes, dtype=torch.uint8, device="cuda")
+        sq.fill_host(kind, key, ctr0, n, host, scratch)
+        want = O.fill_strided(kind, [key], ctr0, 1, n)[0]
+        got = host.numpy()[: n * es].view(want.dtype)
+        assert np.array_equal(got, want), (kind, pinned, first_mismatch(got, want))
+        assert (host.numpy()[n * es:] == 0).all()
