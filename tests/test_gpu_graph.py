@@ -54,3 +54,42 @@ def test_capture_and_replay(sq):
         assert np.array_equal(out_f.cpu().numpy().view(np.uint32), want_f)
         assert np.array_equal(hist.cpu().numpy().view(np.uint64), want_h)
         assert np.array_equal(ones.cpu().numpy().view(np.uint64), want_o)
+
+
+def test_concurrent_host_threads_and_streams(sq):
+    """Reentrancy (include/squares.h): 4 host threads, each with its own CUDA stream, issue fills
+    and fused statistics concurrently (first-call caches included: a fresh process path is not
+    needed, the caches are per device and atomic); every result equals the oracle."""
+    import threading
+    n = (1 << 18) + 3
+    keys = [int(k) for k in O.keygen(21, 4)]
+    results, errors = {}, []
+
+    def work(t):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                outs = []
+                for rep in range(5):
+                    kind = ("u32", "u64", "f32")[(t + rep) % 3]
+                    outs.append((kind, rep, getattr(sq, f"fill_{kind}_k")(keys[t], rep * n, n, stream=s)))
+                h, o = sq.fused_stats(keys[t], 7, n, stream=s)
+            s.synchronize()
+            results[t] = (outs, h.cpu().numpy().view(np.uint64), o.cpu().numpy().view(np.uint64))
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    ths = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert not errors, errors
+    for t in range(4):
+        outs, h, o = results[t]
+        for kind, rep, out in outs:
+            want = O.fill(kind, [keys[t]], rep * n, n)[0]
+            got = out.cpu().numpy().view(want.dtype)
+            assert np.array_equal(got, want), (t, kind, rep)
+        hw, ow = O.fused_stats(keys[t], 7, n)
+        assert np.array_equal(h, hw) and np.array_equal(o, ow), t
