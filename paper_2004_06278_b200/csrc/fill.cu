@@ -70,7 +70,8 @@ __device__ __forceinline__ RowConst<SPL> row_const(uint64_t key, uint64_t stride
 
 // Output words of one sample j of kind KIND into v (little-endian 64-bit elements).
 // Cross-term form (squares_dev.cuh cross_add) per output kind, measured on B200
-// (DESIGN.md 7.5): the funnel-shift doubling (3) for the u32 fill, the plain form (0) else.
+// (DESIGN.md 7.5): the funnel-shift doubling (3) for the 32-bit kinds (u32, f32), the plain
+// form (0) for the squares64 kinds (store-bound).
 #ifndef SQ_FILL_FORM
 #define SQ_FILL_FORM -1
 #endif
@@ -78,7 +79,9 @@ __device__ __forceinline__ RowConst<SPL> row_const(uint64_t key, uint64_t stride
 #define SQ_FILL_FMUL2 1   // f32 scale as a packed FMUL2 over word pairs (gen_lane)
 #endif
 template <int KIND>
-__host__ __device__ constexpr int fill_form() { return SQ_FILL_FORM >= 0 ? SQ_FILL_FORM : (KIND == KIND_U32 ? 3 : 0); }
+__host__ __device__ constexpr int fill_form() {
+  return SQ_FILL_FORM >= 0 ? SQ_FILL_FORM : ((KIND == KIND_U32 || KIND == KIND_F32) ? 3 : 0);
+}
 template <int KIND, int FORM, int NW>
 __device__ __forceinline__ void put(uint32_t (&v)[NW], int j, uint64_t y, uint64_t z, uint64_t u, uint32_t one) {
   if (KIND == KIND_U32 || KIND == KIND_F32) {
