@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, key, ctr0, n, nkeys, q):
+def _worker(rank, world, port, key, ctr0, n, nkeys, q, perm=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     tdist.init_process_group("gloo", rank=rank, world_size=world)
@@ -34,7 +34,11 @@ def _worker(rank, world, port, key, ctr0, n, nkeys, q):
             h, o = O.fused_stats(k, c0, ln)
             return torch.from_numpy(h.view(np.int64).copy()), torch.from_numpy(o.view(np.int64).copy())
 
-        hist, ones = D.fused_stats_sharded(key, ctr0, n, local=local)
+        if perm is None:
+            hist, ones = D.fused_stats_sharded(key, ctr0, n, local=local)
+        else:   # permuted rank -> shard map: rank r computes shard perm[r], then the one all-reduce
+            s0, sl = D.partition(n, world, perm[rank])
+            hist, ones = D.allreduce_counts(*local(key, (ctr0 + s0) & ((1 << 64) - 1), sl))
         c0, ln = D.counter_shard(ctr0, n)
         k0, kn = D.key_shard(nkeys)
         # every rank gets the same reduced counts; report the shard geometry too
@@ -43,14 +47,16 @@ def _worker(rank, world, port, key, ctr0, n, nkeys, q):
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_fused_sharded_allreduce_matches_single(world):
+@pytest.mark.parametrize("world,perm", [(2, None), (3, None), (4, None), (8, None), (4, (2, 0, 3, 1))])
+def test_fused_sharded_allreduce_matches_single(world, perm):
+    """P = 2, 3, 4, 8 ranks (and a permuted rank -> shard map): the all-reduced counts equal the
+    single-process oracle bit for bit, and the shards tile the counter range."""
     key = int(O.keygen(1, 1)[0])
     ctr0, n, nkeys = (1 << 64) - 50_000, 300_001, 10   # shards straddle the 2^64 wrap; ragged
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, key, ctr0, n, nkeys, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, key, ctr0, n, nkeys, q, perm)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]
