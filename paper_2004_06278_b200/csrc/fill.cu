@@ -162,6 +162,20 @@ __device__ __forceinline__ void gen_lane(const State& s, const RowConst<SPL>& rc
   if (KIND == KIND_F32 && SQ_FILL_FMUL2) scale_f32_pairs(v);
 }
 
+// SQ_DEBUG_BOUNDS builds (tests only: SQ_LIB=<debug build> pytest -m gpu) trap any store
+// outside row `row`'s written span [row*ld, row*ld + n) elements -- a stronger check than the
+// tests' sentinel guards, since compute-sanitizer is unavailable on this pool.
+#ifdef SQ_DEBUG_BOUNDS
+#define SQ_CHECK_STORE(a, row, ptr, bytes)                                                       \
+  do {                                                                                         \
+    const char* lo_ = (a).out + (row) * (a).ld_bytes;                                          \
+    const char* hi_ = lo_ + (a).n * (uint64_t)(FillTraits<KIND>::ES);                           \
+    if ((const char*)(ptr) < lo_ || (const char*)(ptr) + (bytes) > hi_) __trap();             \
+  } while (0)
+#else
+#define SQ_CHECK_STORE(a, row, ptr, bytes) do { } while (0)
+#endif
+
 // KEYIMM: a single row whose key is a kernel parameter, so ptxas can keep the key and the
 // per-row constants in uniform registers (sq_fill_*_k).  Otherwise keys[row] from memory.
 template <int KIND, bool KEYIMM, bool STRIDED>
@@ -214,7 +228,10 @@ __global__ void __launch_bounds__(kFillThreads, KEYIMM ? kFillMinBlocksImm : kFi
           for (int j = 0; j < FillTraits<KIND>::W; j++) nostore_acc ^= v[j];
 #else
 #pragma unroll
-          for (int q = 0; q < FillTraits<KIND>::W / 8; q++) st256(p + 32 * q, v + 8 * q);
+          for (int q = 0; q < FillTraits<KIND>::W / 8; q++) {
+            SQ_CHECK_STORE(a, row, p + 32 * q, 32);
+            st256(p + 32 * q, v + 8 * q);
+          }
 #endif
           jump<LOGJ>(s, rc.jk, rc.cj, rc.dj);
           p += J * ES;
@@ -227,6 +244,7 @@ __global__ void __launch_bounds__(kFillThreads, KEYIMM ? kFillMinBlocksImm : kFi
         for (int j = 0; j < SPL; j++) {
           const uint64_t idx = i0 + j;
           if ((int64_t)idx >= 0 && idx < a.n) {
+            SQ_CHECK_STORE(a, row, p + j * ES, ES);
             if (ES == 4) *(uint32_t*)(p + j * 4) = v[j];
             else *(uint64_t*)(p + j * 8) = ((uint64_t)v[2 * j + 1] << 32) | v[2 * j];
           }
