@@ -256,6 +256,20 @@ def test_fused_hot_bins_accumulate_in_pieces(sq, key):
     assert np.array_equal(o.cpu().numpy().view(np.uint64), ow)
 
 
+def test_fused_sweeps_at_scale(sq):
+    """Many sweeps per CTA: key = 2^32 (outputs concentrated on few bins for small counters,
+    closed-form family) over 2^30 counters vs the parallel oracle, and key = 0 over 2^32
+    counters (every sample in bin 0: a sweep at almost every epoch barrier) vs its closed form."""
+    n = 1 << 30
+    h, o = _fused(sq, 1 << 32, 0, n)
+    hw, ow = par_fused(1 << 32, 0, n)
+    assert np.array_equal(h, hw), first_mismatch(h, hw)
+    assert np.array_equal(o, ow), first_mismatch(o, ow)
+    n0 = 1 << 32
+    h0, o0 = _fused(sq, 0, 12345, n0)
+    assert int(h0[0]) == n0 and int(h0[1:].sum()) == 0 and int(o0.sum()) == 0
+
+
 def test_fused_2_30_vs_parallel_oracle(sq):
     key = int(O.keygen(1, 1)[0])
     n = 1 << 30
