@@ -41,9 +41,18 @@ __global__ void __launch_bounds__(256) keyctr_kernel(const uint64_t* __restrict_
   const uint64_t groups = nkeys / 4;
   const bool vec = (((uintptr_t)keys | (uintptr_t)out) & 15) == 0;   // 16-byte aligned arrays
   if (vec) {
+    // the next group's keys are loaded before the current group's arithmetic (prefetch)
+    ulonglong2 na = make_ulonglong2(0, 0), nb = na;
+    if (tid < groups) {
+      na = __ldg((const ulonglong2*)(keys + 4 * tid));
+      nb = __ldg((const ulonglong2*)(keys + 4 * tid + 2));
+    }
     for (uint64_t g = tid; g < groups; g += T) {
-      const ulonglong2 a = __ldg((const ulonglong2*)(keys + 4 * g));
-      const ulonglong2 b = __ldg((const ulonglong2*)(keys + 4 * g + 2));
+      const ulonglong2 a = na, b = nb;
+      if (g + T < groups) {
+        na = __ldg((const ulonglong2*)(keys + 4 * (g + T)));
+        nb = __ldg((const ulonglong2*)(keys + 4 * (g + T) + 2));
+      }
       const uint64_t v0 = keyctr_value<KIND>(ctr, a.x), v1 = keyctr_value<KIND>(ctr, a.y);
       const uint64_t v2 = keyctr_value<KIND>(ctr, b.x), v3 = keyctr_value<KIND>(ctr, b.y);
       if (ES == 4) {
