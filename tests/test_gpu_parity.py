@@ -7,6 +7,8 @@ product.  Sizes: small cases span several warp chunks and ragged tails; the full
 BASELINE.json (c2, c3, c4) are compared in full against the oracle run on all host cores; c5
 (2^38 counters) is checked by invariants plus oracle parity on sampled sub-ranges.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -298,6 +300,20 @@ def test_fused_c5_full_size(sq):
         hs, os_ = _fused(sq, key, start, 1 << 24)
         hw, ow = par_fused(key, start, 1 << 24)
         assert np.array_equal(hs, hw) and np.array_equal(os_, ow), start
+
+
+@pytest.mark.skipif(os.environ.get("SQ_FULL_ORACLE") != "1",
+                    reason="~6 min of host CPU: run with SQ_FULL_ORACLE=1 (log: profiles/r01_c5_full_oracle_pytest.log)")
+def test_fused_c5_full_size_vs_full_oracle(sq):
+    """BASELINE.json config 5 at its full size (2^38 counters) against the oracle run over the
+    WHOLE range on all host cores (337 s on the 16-core GPU host): every histogram bin and every
+    per-bit count bit-exact, not only the invariants and sampled sub-ranges of the default run."""
+    w = SI.CONFIGS["c5"]
+    key = int(O.keygen(w.key_seed, 1)[0])
+    h, o = _fused(sq, key, w.ctr0, w.n)
+    hw, ow = par_fused(key, w.ctr0, w.n)
+    assert np.array_equal(h, hw), first_mismatch(h, hw)
+    assert np.array_equal(o, ow), first_mismatch(o, ow)
 
 
 def test_fill_host_e2e(sq):
