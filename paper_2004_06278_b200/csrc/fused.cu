@@ -233,10 +233,6 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
   uint32_t pl[kPlanes];
 #pragma unroll
   for (int p = 0; p < kPlanes; p++) pl[p] = 0;
-  uint32_t colcnt[16];
-#pragma unroll
-  for (int j = 0; j < 16; j++) colcnt[j] = 0;
-
   uint64_t done = 0;
   int since_flush = 0;
   for (uint32_t ep = 0; ep < epochs; ep++) {
@@ -263,6 +259,7 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
     if (++since_flush == kFlushEvery) {   // planes hold <= 63 per column: flush to the CTA totals
       since_flush = 0;
 #pragma unroll
+      uint32_t colcnt[16] = {};   // transient: nothing column-wise lives across the loop
       for (int p = 0; p < kPlanes; p++) { columns_add(colcnt, pl[p], 16u << p); pl[p] = 0; }
       warp_flush16(colcnt, lo_cnt);
     }
@@ -279,6 +276,7 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
     }
   }
   // remaining carry-save state: weights 1, 2, 4, 8 and the planes
+  uint32_t colcnt[16] = {};
   columns_add(colcnt, ones, 1);
   columns_add(colcnt, twos, 2);
   columns_add(colcnt, fours, 4);
