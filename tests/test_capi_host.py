@@ -91,6 +91,36 @@ def test_fill_argument_errors_without_device(sq):
     assert lib.sq_fill_host(0, 1, 0, 5, 0x1000, 0x2000, 16, None, None) == sq.SQ_EINVAL
 
 
+def test_extended_entry_points_argument_errors_without_device(sq):
+    """The 8(f) entry points validate before any CUDA call (CPU-only box): bad kind / stride /
+    flags / width / alignment -> SQ_EINVAL, empty work -> SQ_OK, too many keys -> SQ_ERANGE."""
+    lib = sq._load()
+    K, O_, H, C = 0x10000, 0x20000, 0x30000, 0x40000
+    # sq_fill_ex(kind, keys, nkeys, key_imm, ctr0, stride, n, out, ld, stream)
+    assert lib.sq_fill_ex(9, K, 1, 0, 0, 1, 10, O_, 10, None) == sq.SQ_EINVAL          # kind
+    assert lib.sq_fill_ex(0, K, 1, 0, 0, 0, 10, O_, 10, None) == sq.SQ_EINVAL          # stride 0
+    assert lib.sq_fill_ex(0, None, 2, 7, 0, 1, 10, O_, 10, None) == sq.SQ_EINVAL       # by value, 2 rows
+    assert lib.sq_fill_ex(1, K, 1, 0, 0, 1, 10, O_ + 4, 10, None) == sq.SQ_EINVAL      # u64 misaligned
+    assert lib.sq_fill_ex(0, K, 1, 0, 0, 3, 0, O_, 0, None) == sq.SQ_OK                # n == 0
+    # sq_fill_keyctr(kind, keys, nkeys, ctr, out, stream)
+    assert lib.sq_fill_keyctr(0, K, 0, 5, O_, None) == sq.SQ_OK
+    assert lib.sq_fill_keyctr(0, None, 3, 5, O_, None) == sq.SQ_EINVAL
+    assert lib.sq_fill_keyctr(0, K + 4, 3, 5, O_, None) == sq.SQ_EINVAL                # keys misaligned
+    assert lib.sq_fill_keyctr(5, K, 3, 5, O_, None) == sq.SQ_EINVAL                    # kind
+    # sq_fused_stats_ex(key, ctr0, stride, n, flags, hist, ones, stream)
+    assert lib.sq_fused_stats_ex(1, 0, 0, 5, 0, H, H, None) == sq.SQ_EINVAL            # stride 0
+    assert lib.sq_fused_stats_ex(1, 0, 1, 5, 2, H, H, None) == sq.SQ_EINVAL            # unknown flag
+    assert lib.sq_fused_stats_ex(1, 0, 1, 0, 1, None, None, None) == sq.SQ_OK
+    # sq_transitions(key, ctr0, stride, n, flags, count, stream)
+    assert lib.sq_transitions(1, 0, 1, 5, 0, C + 4, None) == sq.SQ_EINVAL              # misaligned
+    assert lib.sq_transitions(1, 0, 1, 0, 0, None, None) == sq.SQ_OK
+    # sq_scaled_hist(W, keys, nkeys, hist, stream)
+    for W in (6, 9, 34):
+        assert lib.sq_scaled_hist(W, K, 1, H, None) == sq.SQ_EINVAL
+    assert lib.sq_scaled_hist(16, K, 0, H, None) == sq.SQ_OK
+    assert lib.sq_scaled_hist(16, K, 65536, H, None) == sq.SQ_ERANGE
+
+
 def test_product_never_imports_oracle():
     """The product path must not reference the oracle (checked textually)."""
     pkg = os.path.join(ROOT, "paper_2004_06278_b200")
