@@ -29,8 +29,10 @@
 //        y += J*key;  u += J*e + J(J-1)*key^2;  e += J*2*key^2,   J*e = e << log2(J).
 //
 // Per squares32 sample: rounds 2-4 = 2 IMAD.WIDE.U32 + 1 IMAD.HI.U32 + 3 IMAD (9 FMA-heavy
-// pipe slots: IMAD 64 lanes/clk/SM, WIDE/HI 32 on B200) plus 3 doublings and the two 64-bit
-// walk adds.  squares64 adds round 4's full sum and round 5.
+// pipe slots: IMAD 64 lanes/clk/SM, WIDE/HI 2 slots each -- 24-27 lanes/clk/SM measured in
+// dependent loops on B200) plus 3 doublings and the two 64-bit walk adds.  squares64 adds
+// round 4's full sum and round 5.  A Stream draw runs at ~1.25 Tsamples/s per B200 when the
+// value is consumed in registers (tools/bench_next.py).
 #pragma once
 #include <stdint.h>
 
@@ -75,6 +77,8 @@ __device__ __forceinline__ uint64_t add64_3(uint64_t a, uint64_t b, uint64_t c) 
 //                                               dependency chain (shorter latency per round)
 //   3  IMAD(xl, SHF(RZ:xh, 1), hi)           -- the doubling as a funnel shift with an immediate
 //                                               amount: ALU pipe, one register read
+// Measured on B200: form 3 is fastest for the library's 32-bit fills (the ALU has room next to
+// the stores), form 0 for compute-only loops (fused statistics, Stream): the default here.
 #ifndef SQ_ROUND_FORM
 #define SQ_ROUND_FORM 0
 #endif
