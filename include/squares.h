@@ -88,7 +88,7 @@ int sq_keygen(uint64_t seed, uint64_t count, uint64_t* keys_host);
  * Bulk fills (BASELINE.json configs 1-4).  Row-major [key][ctr] layout:
  *   out[k*ld + i] = G(ctr0 + i mod 2^64, keys[k])   for k < nkeys, i < n;
  * elements i in [n, ld) of each row are left untouched.
- *   keys_dev  device, nkeys uint64 keys (read only)
+ *   keys_dev  device, nkeys uint64 keys (read only), 8-byte aligned
  *   nkeys     number of rows
  *   ctr0      first counter of every row
  *   n         counters per row
@@ -97,7 +97,7 @@ int sq_keygen(uint64_t seed, uint64_t count, uint64_t* keys_host);
  *             nkeys == 1)
  * Returns SQ_OK without launching when n == 0 or nkeys == 0.
  * Errors: SQ_EINVAL on NULL pointers with work to do, ld < n with nkeys > 1, a misaligned
- * out_dev, or nkeys*ld*elem overflowing size_t; SQ_ECUDA if the launch fails.
+ * out_dev or keys_dev, or nkeys*ld*elem overflowing size_t; SQ_ECUDA if the launch fails.
  * -------------------------------------------------------------------------------------- */
 
 /* G = squares32, uint32 output. */
@@ -216,8 +216,11 @@ int sq_scaled_hist(int W, const uint64_t* keys_dev, uint64_t nkeys, uint64_t* hi
  * (cudaHostAlloc / cudaHostRegister) for full PCIe bandwidth.
  *   kind        SQ_KIND_* (0 = u32, 1 = u64, 2 = f32, 3 = f64, 4 = f32x2)
  *   key         the key (host value)
- *   scratch_dev device scratch, >= 2 * 32 bytes, 256-byte aligned recommended
- * Errors: SQ_EINVAL (bad kind, NULL pointers with n > 0, scratch too small), SQ_ECUDA.
+ *   scratch_dev device scratch, aligned to the element size; the library starts its two
+ *               halves at the first 32-byte boundary inside it, so it needs >= 2 * 32 bytes
+ *               plus that offset (256-byte aligned recommended)
+ * Errors: SQ_EINVAL (bad kind, NULL pointers with n > 0, scratch misaligned to the element
+ * size or too small), SQ_ECUDA.
  * -------------------------------------------------------------------------------------- */
 int sq_fill_host(int kind, uint64_t key, uint64_t ctr0, uint64_t n, void* out_host,
                  void* scratch_dev, size_t scratch_bytes, sq_stream_t stream,

@@ -21,8 +21,10 @@
  *   fill_* / f32          : per-element definition; f32 exact examples (0, 2^-24, 0.5, 1-2^-24).
  *   fused_stats           : key = 0 closed form, sum(hist) = n, ones[16+j] from hist,
  *       additivity over shards, equality with fill_u32 + numpy.bincount.
- *   scaled analogue       : W = 64 equals squares32; key 0 -> constant 0; chi^2 p-value
- *       numerics against scipy.special.gammaincc.
+ *   scaled analogue       : hand-derived W = 8 and W = 16 values (tests/golden/scaled_values.txt);
+ *       W = 64 equals squares32; key 0 -> constant 0; chi^2 p-value numerics against
+ *       scipy.special.gammaincc.
+ *   xorfold_u32           : n = 1 hand value, key 0 -> 0, the same fold of fill_u32 in numpy.
  *   partition             : SPEC examples, disjointness and coverage.
  *   validate_key          : SPEC examples and the rules of P:37.
  *   keygen                : rules, determinism, prefix stability, distinctness.

@@ -98,14 +98,55 @@ def _check(fn: str, code: int) -> None:
         raise SquaresError(fn, code)
 
 
-def _stream_handle(stream) -> int:
+def _device(dev) -> torch.device:
+    """A concrete CUDA device (index resolved) from a tensor device, a string or None."""
+    d = torch.device(dev if dev is not None else "cuda")
+    if d.type != "cuda":
+        raise ValueError(f"expected a CUDA device, got {d}")
+    return torch.device("cuda", torch.cuda.current_device() if d.index is None else d.index)
+
+
+def _stream_handle(stream, device: torch.device | None = None) -> int:
+    """The raw stream the library launches on: `stream`, else `device`'s current stream.  The
+    C ABI launches on the CURRENT device, so every entry point below runs inside
+    `torch.cuda.device(device)` and a stream of another device is rejected."""
     if stream is None:
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(device)
+    elif device is not None and stream.device != device:
+        raise ValueError(f"stream is on {stream.device}, tensors on {device}")
     return stream.cuda_stream
 
 
 def _u64(x: int) -> int:
     return int(x) & M64
+
+
+def _count(n: int, what: str = "n") -> int:
+    """A count argument of the C ABI (uint64): 0 <= n < 2^64, else ValueError (ctypes would
+    silently reduce it mod 2^64)."""
+    n = int(n)
+    if not 0 <= n <= M64:
+        raise ValueError(f"{what} = {n} is outside [0, 2^64)")
+    return n
+
+
+def _check_keys(keys: torch.Tensor) -> torch.device:
+    if not (isinstance(keys, torch.Tensor) and keys.is_cuda and keys.dtype == torch.int64 and keys.dim() == 1
+            and keys.is_contiguous()):
+        raise ValueError("keys must be a contiguous 1-D int64 CUDA tensor")
+    return _device(keys.device)
+
+
+def _check_counts(t: torch.Tensor, numel: int, name: str, device: torch.device | None) -> torch.device:
+    """Caller-supplied accumulators (hist / ones / count): the kernels atomically add to exactly
+    `numel` uint64 entries, so anything else would be an out-of-bounds device write."""
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.int64 and t.numel() == numel
+            and t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous int64 CUDA tensor of {numel} elements")
+    d = _device(t.device)
+    if device is not None and d != device:
+        raise ValueError(f"{name} is on {d}, expected {device}")
+    return d
 
 
 # ----------------------------------------------------------------------------- host functions
@@ -120,8 +161,11 @@ def validate_key(key: int) -> int:
 
 def keygen(seed: int, count: int) -> torch.Tensor:
     """`count` keys of stream `seed` (documented "different digits" mapping), int64 CPU tensor."""
-    out = torch.empty(max(int(count), 1), dtype=torch.int64)
-    _check("sq_keygen", _load().sq_keygen(_u64(seed), int(count), out.data_ptr()))
+    count = _count(count, "count")
+    if count > (1 << 31):   # the library's SQ_ERANGE, checked before allocating count keys
+        raise SquaresError("sq_keygen", SQ_ERANGE)
+    out = torch.empty(max(count, 1), dtype=torch.int64)
+    _check("sq_keygen", _load().sq_keygen(_u64(seed), count, out.data_ptr()))
     return out[: int(count)]
 
 
@@ -143,37 +187,57 @@ def _elems(kind, t: torch.Tensor) -> int:
     return t.numel() * t.element_size() // _ELEM_BYTES[kind]
 
 
+def _check_out(kind: str, out: torch.Tensor, need: int, device: torch.device) -> None:
+    if not (isinstance(out, torch.Tensor) and out.dtype == _OUT_DTYPE[kind] and out.is_cuda
+            and out.is_contiguous()):
+        raise ValueError(f"out must be a contiguous CUDA {_OUT_DTYPE[kind]} tensor")
+    if _device(out.device) != device:
+        raise ValueError(f"out is on {out.device}, expected {device}")
+    if _elems(kind, out) < need:
+        raise ValueError(f"out holds {_elems(kind, out)} elements, {need} needed")
+
+
+def _infer_ld(kind: str, out: torch.Tensor | None, ld: int | None, n: int) -> int:
+    """Row pitch: explicit `ld`, else the row length of a 2-D out (3-D for f32x2), else n."""
+    if ld is not None:
+        return _count(ld, "ld")
+    nd = 3 if kind == "f32x2" else 2
+    if out is not None and out.dim() == nd:
+        return int(out.shape[1])
+    return n
+
+
 def _fill(kind: str, keys: torch.Tensor, ctr0: int, n: int, out: torch.Tensor | None, ld: int | None,
           stream=None) -> torch.Tensor:
-    if not (keys.is_cuda and keys.dtype == torch.int64 and keys.dim() == 1 and keys.is_contiguous()):
-        raise ValueError("keys must be a contiguous 1-D int64 CUDA tensor")
+    dev = _check_keys(keys)
+    n = _count(n)
     nkeys = keys.numel()
+    ld = _infer_ld(kind, out, ld, n)
     if out is None:
-        ld = n if ld is None else ld
-        out = _alloc(kind, (nkeys, ld), keys.device)
+        out = _alloc(kind, (nkeys, ld), dev)
     else:
-        if out.dtype != _OUT_DTYPE[kind] or not out.is_cuda:
-            raise ValueError(f"out must be a CUDA {_OUT_DTYPE[kind]} tensor")
-        if ld is None:
-            nd = 3 if kind == "f32x2" else 2
-            ld = out.shape[1] if out.dim() == nd else n
-        need = (nkeys - 1) * ld + n if nkeys else 0
-        if _elems(kind, out) < need or not out.is_contiguous():
-            raise ValueError("out is too small or not contiguous")
+        _check_out(kind, out, (nkeys - 1) * ld + n if nkeys else 0, dev)
     fn = getattr(_load(), f"sq_fill_{kind}")
-    _check(f"sq_fill_{kind}", fn(keys.data_ptr(), nkeys, _u64(ctr0), int(n), out.data_ptr(), int(ld),
-                                 _stream_handle(stream)))
+    with torch.cuda.device(dev):
+        _check(f"sq_fill_{kind}", fn(keys.data_ptr(), nkeys, _u64(ctr0), n, out.data_ptr(), ld,
+                                     _stream_handle(stream, dev)))
     return out
 
 
 def _fill_k(kind: str, key: int, ctr0: int, n: int, out: torch.Tensor | None, device=None,
             stream=None) -> torch.Tensor:
+    n = _count(n)
     if out is None:
-        out = _alloc(kind, (int(n),), device if device is not None else "cuda")
-    elif out.dtype != _OUT_DTYPE[kind] or not out.is_cuda or not out.is_contiguous() or _elems(kind, out) < n:
-        raise ValueError(f"out must be a contiguous CUDA {_OUT_DTYPE[kind]} tensor of >= n elements")
+        dev = _device(device)
+        out = _alloc(kind, (n,), dev)
+    else:
+        dev = _device(out.device)
+        if device is not None and _device(device) != dev:
+            raise ValueError(f"out is on {dev}, device={device}")
+        _check_out(kind, out, n, dev)
     fn = getattr(_load(), f"sq_fill_{kind}_k")
-    _check(f"sq_fill_{kind}_k", fn(_u64(key), _u64(ctr0), int(n), out.data_ptr(), _stream_handle(stream)))
+    with torch.cuda.device(dev):
+        _check(f"sq_fill_{kind}_k", fn(_u64(key), _u64(ctr0), n, out.data_ptr(), _stream_handle(stream, dev)))
     return out
 
 
@@ -233,69 +297,96 @@ def fill_ex(kind: str, ctr0: int, n: int, stride: int = 1, keys: torch.Tensor | 
     (rows) or one key by value."""
     if (keys is None) == (key is None):
         raise ValueError("pass exactly one of keys (device tensor) or key (int)")
+    n = _count(n)
     if keys is not None:
-        if not (keys.is_cuda and keys.dtype == torch.int64 and keys.dim() == 1 and keys.is_contiguous()):
-            raise ValueError("keys must be a contiguous 1-D int64 CUDA tensor")
-        nkeys, kptr, kimm, dev = keys.numel(), keys.data_ptr(), 0, keys.device
+        dev = _check_keys(keys)
+        nkeys, kptr, kimm = keys.numel(), keys.data_ptr(), 0
     else:
-        nkeys, kptr, kimm, dev = 1, None, _u64(key), (device if device is not None else "cuda")
-    ld = n if ld is None else ld
+        dev = _device(out.device if out is not None and device is None else device)
+        nkeys, kptr, kimm = 1, None, _u64(key)
+    ld = _infer_ld(kind, out, ld, n)
     if out is None:
         out = _alloc(kind, (nkeys, ld), dev)
-    elif out.dtype != _OUT_DTYPE[kind] or not out.is_cuda or not out.is_contiguous() or \
-            _elems(kind, out) < (nkeys - 1) * ld + n:
-        raise ValueError("bad out tensor")
-    _check("sq_fill_ex", _load().sq_fill_ex(KINDS[kind], kptr, nkeys, kimm, _u64(ctr0), _u64(stride), int(n),
-                                            out.data_ptr(), int(ld), _stream_handle(stream)))
+    else:
+        _check_out(kind, out, (nkeys - 1) * ld + n if nkeys else 0, dev)
+    with torch.cuda.device(dev):
+        _check("sq_fill_ex", _load().sq_fill_ex(KINDS[kind], kptr, nkeys, kimm, _u64(ctr0), _u64(stride), n,
+                                                out.data_ptr(), ld, _stream_handle(stream, dev)))
     return out
 
 
 def fill_keyctr(kind: str, keys: torch.Tensor, ctr: int, out: torch.Tensor | None = None, stream=None):
     """Key-counter mode: out[j] = G(ctr, keys[j])."""
-    if not (keys.is_cuda and keys.dtype == torch.int64 and keys.dim() == 1 and keys.is_contiguous()):
-        raise ValueError("keys must be a contiguous 1-D int64 CUDA tensor")
+    dev = _check_keys(keys)
     if out is None:
-        out = _alloc(kind, (keys.numel(),), keys.device)
-    elif out.dtype != _OUT_DTYPE[kind] or not out.is_cuda or not out.is_contiguous() or \
-            _elems(kind, out) < keys.numel():
-        raise ValueError("bad out tensor")
-    _check("sq_fill_keyctr", _load().sq_fill_keyctr(KINDS[kind], keys.data_ptr(), keys.numel(), _u64(ctr),
-                                                    out.data_ptr(), _stream_handle(stream)))
+        out = _alloc(kind, (keys.numel(),), dev)
+    else:
+        _check_out(kind, out, keys.numel(), dev)
+    with torch.cuda.device(dev):
+        _check("sq_fill_keyctr", _load().sq_fill_keyctr(KINDS[kind], keys.data_ptr(), keys.numel(), _u64(ctr),
+                                                        out.data_ptr(), _stream_handle(stream, dev)))
     return out
+
+
+def _counts_pair(hist, ones, device):
+    """(hist, ones, device): allocated zeroed on `device` when None, else validated."""
+    dev = None
+    if hist is not None:
+        dev = _check_counts(hist, HIST_BINS, "hist", None)
+    if ones is not None:
+        dev = _check_counts(ones, 32, "ones", dev)
+    if dev is None:
+        dev = _device(device)
+    elif device is not None and _device(device) != dev:
+        raise ValueError(f"counts are on {dev}, device={device}")
+    if hist is None:
+        hist = torch.zeros(HIST_BINS, dtype=torch.int64, device=dev)
+    if ones is None:
+        ones = torch.zeros(32, dtype=torch.int64, device=dev)
+    return hist, ones, dev
 
 
 def fused_stats_ex(key: int, ctr0: int, n: int, stride: int = 1, bitrev: bool = False,
                    hist: torch.Tensor | None = None, ones: torch.Tensor | None = None, device=None, stream=None):
     """Fused statistics over counters ctr0 + i*stride, optionally of bit-reversed outputs."""
-    dev = device if device is not None else (hist.device if hist is not None else torch.device("cuda"))
-    hist = torch.zeros(HIST_BINS, dtype=torch.int64, device=dev) if hist is None else hist
-    ones = torch.zeros(32, dtype=torch.int64, device=dev) if ones is None else ones
-    _check("sq_fused_stats_ex", _load().sq_fused_stats_ex(_u64(key), _u64(ctr0), _u64(stride), int(n),
-                                                          SQ_FUSED_BITREV if bitrev else 0, hist.data_ptr(),
-                                                          ones.data_ptr(), _stream_handle(stream)))
+    n = _count(n)
+    hist, ones, dev = _counts_pair(hist, ones, device)
+    with torch.cuda.device(dev):
+        _check("sq_fused_stats_ex", _load().sq_fused_stats_ex(_u64(key), _u64(ctr0), _u64(stride), n,
+                                                              SQ_FUSED_BITREV if bitrev else 0, hist.data_ptr(),
+                                                              ones.data_ptr(), _stream_handle(stream, dev)))
     return hist, ones
 
 
 def transitions(key: int, ctr0: int, n: int, stride: int = 1, bitrev: bool = False,
                 count: torch.Tensor | None = None, device=None, stream=None) -> torch.Tensor:
     """Accumulate the number of adjacent differing bits of the LSB-first output bit stream."""
-    dev = device if device is not None else (count.device if count is not None else torch.device("cuda"))
-    count = torch.zeros(1, dtype=torch.int64, device=dev) if count is None else count
-    _check("sq_transitions", _load().sq_transitions(_u64(key), _u64(ctr0), _u64(stride), int(n),
-                                                    SQ_FUSED_BITREV if bitrev else 0, count.data_ptr(),
-                                                    _stream_handle(stream)))
+    n = _count(n)
+    if count is None:
+        dev = _device(device)
+        count = torch.zeros(1, dtype=torch.int64, device=dev)
+    else:
+        dev = _check_counts(count, 1, "count", _device(device) if device is not None else None)
+    with torch.cuda.device(dev):
+        _check("sq_transitions", _load().sq_transitions(_u64(key), _u64(ctr0), _u64(stride), n,
+                                                        SQ_FUSED_BITREV if bitrev else 0, count.data_ptr(),
+                                                        _stream_handle(stream, dev)))
     return count
 
 
 def scaled_hist(W: int, keys: torch.Tensor, hist: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Exhaustive W-bit uniformity histograms, shape (nkeys, 2^(W/2)) int64 (accumulating)."""
-    if not (keys.is_cuda and keys.dtype == torch.int64 and keys.dim() == 1 and keys.is_contiguous()):
-        raise ValueError("keys must be a contiguous 1-D int64 CUDA tensor")
+    dev = _check_keys(keys)
+    if not (isinstance(W, int) and 8 <= W <= 32 and W % 2 == 0):
+        raise ValueError("W must be an even integer in [8, 32]")
     nb = 1 << (W // 2)
     if hist is None:
-        hist = torch.zeros((keys.numel(), nb), dtype=torch.int64, device=keys.device)
-    _check("sq_scaled_hist", _load().sq_scaled_hist(int(W), keys.data_ptr(), keys.numel(), hist.data_ptr(),
-                                                    _stream_handle(stream)))
+        hist = torch.zeros((keys.numel(), nb), dtype=torch.int64, device=dev)
+    else:
+        _check_counts(hist, keys.numel() * nb, "hist", dev)
+    with torch.cuda.device(dev):
+        _check("sq_scaled_hist", _load().sq_scaled_hist(int(W), keys.data_ptr(), keys.numel(), hist.data_ptr(),
+                                                        _stream_handle(stream, dev)))
     return hist
 
 
@@ -303,16 +394,11 @@ def fused_stats(key: int, ctr0: int, n: int, hist: torch.Tensor | None = None,
                 ones: torch.Tensor | None = None, device=None, stream=None):
     """Accumulate the top-16-bit histogram (65536 bins) and the 32 per-bit ones counts of
     squares32 over [ctr0, ctr0 + n) into int64 CUDA tensors (allocated zeroed if None)."""
-    dev = device if device is not None else (hist.device if hist is not None else torch.device("cuda"))
-    if hist is None:
-        hist = torch.zeros(HIST_BINS, dtype=torch.int64, device=dev)
-    if ones is None:
-        ones = torch.zeros(32, dtype=torch.int64, device=dev)
-    for t, sz in ((hist, HIST_BINS), (ones, 32)):
-        if not (t.is_cuda and t.dtype == torch.int64 and t.numel() == sz and t.is_contiguous()):
-            raise ValueError(f"expected a contiguous int64 CUDA tensor of {sz} elements")
-    _check("sq_fused_stats", _load().sq_fused_stats(_u64(key), _u64(ctr0), int(n), hist.data_ptr(),
-                                                    ones.data_ptr(), _stream_handle(stream)))
+    n = _count(n)
+    hist, ones, dev = _counts_pair(hist, ones, device)
+    with torch.cuda.device(dev):
+        _check("sq_fused_stats", _load().sq_fused_stats(_u64(key), _u64(ctr0), n, hist.data_ptr(),
+                                                        ones.data_ptr(), _stream_handle(stream, dev)))
     return hist, ones
 
 
@@ -320,16 +406,19 @@ def fill_host(kind: str, key: int, ctr0: int, n: int, out_host: torch.Tensor, sc
               stream=None, copy_stream=None) -> torch.Tensor:
     """End-to-end fill of ONE key into a (pinned) host tensor via the library's chunked
     generate + D2H pipeline.  Synchronous."""
+    n = _count(n)
     es = _ELEM_BYTES[kind]
     if out_host.is_cuda or out_host.numel() * out_host.element_size() < n * es:
         raise ValueError("out_host must be a host tensor of at least n elements")
-    if not scratch.is_cuda:
-        raise ValueError("scratch must be a CUDA tensor")
-    cs = _stream_handle(copy_stream) if copy_stream is not None else None
-    _check("sq_fill_host", _load().sq_fill_host(KINDS[kind], _u64(key), _u64(ctr0), int(n),
-                                                out_host.data_ptr(), scratch.data_ptr(),
-                                                scratch.numel() * scratch.element_size(),
-                                                _stream_handle(stream), cs))
+    if not (scratch.is_cuda and scratch.is_contiguous()):
+        raise ValueError("scratch must be a contiguous CUDA tensor")
+    dev = _device(scratch.device)
+    with torch.cuda.device(dev):
+        cs = _stream_handle(copy_stream, dev) if copy_stream is not None else None
+        _check("sq_fill_host", _load().sq_fill_host(KINDS[kind], _u64(key), _u64(ctr0), n,
+                                                    out_host.data_ptr(), scratch.data_ptr(),
+                                                    scratch.numel() * scratch.element_size(),
+                                                    _stream_handle(stream, dev), cs))
     return out_host
 
 

@@ -57,6 +57,7 @@ static int fill_any(int kind, const uint64_t* keys_dev, uint64_t nkeys, uint64_t
   if (!out_dev) return SQ_EINVAL;
   if (!keys_dev && nkeys != 1) return SQ_EINVAL;
   if (((uintptr_t)out_dev % es) != 0) return SQ_EINVAL;
+  if (((uintptr_t)keys_dev & 7) != 0) return SQ_EINVAL;   // the kernels __ldg 8-byte keys
   if (nkeys == 1) ld = n;
   if (ld < n) return SQ_EINVAL;
   if (!size_ok(nkeys, ld, es)) return SQ_EINVAL;
@@ -199,7 +200,14 @@ int sq_fill_host(int kind, uint64_t key, uint64_t ctr0, uint64_t n, void* out_ho
   if (n == 0) return SQ_OK;
   if (!out_host || !scratch_dev) return SQ_EINVAL;
   const uint64_t es = kind_elem_bytes(kind);
-  // two ping-pong halves, each a multiple of 32 bytes
+  // the fill kernel corrects misalignment only in whole elements: an unaligned scratch
+  // pointer would make its 256-bit stores fault (a sticky context error), so reject it
+  if (((uintptr_t)scratch_dev % es) != 0) return SQ_EINVAL;
+  // two ping-pong halves, each a multiple of 32 bytes, the first starting 32-byte aligned
+  const uint64_t pad = (32 - ((uintptr_t)scratch_dev & 31)) & 31;
+  if (scratch_bytes < pad) return SQ_EINVAL;
+  scratch_dev = (char*)scratch_dev + pad;
+  scratch_bytes -= pad;
   const uint64_t half = (scratch_bytes / 2) & ~(uint64_t)31;
   const uint64_t chunk = half / es;
   if (chunk == 0) return SQ_EINVAL;

@@ -21,7 +21,8 @@ HIST_BINS = 65536
 
 def partition(n: int, parts: int, idx: int) -> tuple[int, int]:
     """(start, length) of part `idx` when [0, n) is divided into `parts` contiguous pieces:
-    floor(n / parts) each, the last absorbing the remainder.  n may be 2^64."""
+    floor(n / parts) each, the last absorbing the remainder.  n may be 2^64
+    (a shard of length 2^64 cannot be passed to the C ABI in one call: the bindings reject it)."""
     if parts < 1 or not (0 <= idx < parts):
         raise ValueError("need parts >= 1 and 0 <= idx < parts")
     q = n // parts
@@ -48,11 +49,34 @@ def key_shard(nkeys: int, group=None) -> tuple[int, int]:
     return partition(nkeys, p, r)
 
 
+def counts_buffer(device=None) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """One zeroed packed int64 buffer of 65,568 counts and its two views (hist = the first
+    65,536, ones = the last 32), so the exchange below runs in place on a single tensor."""
+    buf = torch.zeros(HIST_BINS + 32, dtype=torch.int64, device=device)
+    return buf, buf[:HIST_BINS], buf[HIST_BINS:]
+
+
+def _packed(hist: torch.Tensor, ones: torch.Tensor) -> torch.Tensor | None:
+    """The packed buffer hist and ones are views of (counts_buffer), else None."""
+    if not (hist.is_contiguous() and ones.is_contiguous() and hist.numel() == HIST_BINS and ones.numel() == 32):
+        return None
+    if hist.untyped_storage().data_ptr() != ones.untyped_storage().data_ptr():
+        return None
+    if ones.data_ptr() != hist.data_ptr() + HIST_BINS * hist.element_size():
+        return None
+    return hist.view(-1).as_strided((HIST_BINS + 32,), (1,))
+
+
 def allreduce_counts(hist: torch.Tensor, ones: torch.Tensor, group=None) -> tuple[torch.Tensor, torch.Tensor]:
-    """SUM-all-reduce hist (65536) and ones (32) int64 counts in ONE collective (one packed
-    65,568-element buffer, 524,544 bytes).  Integer addition is associative and commutative, so
-    the result is bit-identical for any world size and rank order."""
+    """SUM-all-reduce hist (65536) and ones (32) int64 counts in ONE collective over one packed
+    65,568-element buffer (524,544 bytes): in place when hist and ones are the two views of
+    counts_buffer(), else through a packed copy.  Integer addition is associative and
+    commutative, so the result is bit-identical for any world size and rank order."""
     if not (tdist.is_available() and tdist.is_initialized()):
+        return hist, ones
+    buf = _packed(hist, ones)
+    if buf is not None:
+        tdist.all_reduce(buf, op=tdist.ReduceOp.SUM, group=group)
         return hist, ones
     buf = torch.cat([hist.reshape(-1), ones.reshape(-1)])
     tdist.all_reduce(buf, op=tdist.ReduceOp.SUM, group=group)
@@ -63,14 +87,16 @@ def allreduce_counts(hist: torch.Tensor, ones: torch.Tensor, group=None) -> tupl
 
 def fused_stats_sharded(key: int, ctr0: int, n: int,
                         local: Callable[[int, int, int], tuple[torch.Tensor, torch.Tensor]] | None = None,
-                        group=None) -> tuple[torch.Tensor, torch.Tensor]:
+                        group=None, device=None) -> tuple[torch.Tensor, torch.Tensor]:
     """Counter-sharded fused statistics: rank r computes its shard with `local(key, c0, ln)`
-    (default: the CUDA kernel via paper_2004_06278_b200.fused_stats), then one all-reduce."""
+    (default: the CUDA kernel, paper_2004_06278_b200.fused_stats, accumulating into one packed
+    counts buffer on `device`), then one in-place all-reduce."""
     if local is None:
         from . import fused_stats as _fused
 
         def local(k, c0, ln):
-            return _fused(k, c0, ln)
+            _, h, o = counts_buffer(device if device is not None else "cuda")
+            return _fused(k, c0, ln, hist=h, ones=o)
     c0, ln = counter_shard(ctr0, n, group)
     hist, ones = local(key, c0, ln)
     return allreduce_counts(hist, ones, group)

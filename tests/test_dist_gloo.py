@@ -32,7 +32,12 @@ def _worker(rank, world, port, key, ctr0, n, nkeys, q, perm=None):
 
         def local(k, c0, ln):
             h, o = O.fused_stats(k, c0, ln)
-            return torch.from_numpy(h.view(np.int64).copy()), torch.from_numpy(o.view(np.int64).copy())
+            if rank % 2:   # odd ranks: separate tensors (the packed-copy path of allreduce_counts)
+                return torch.from_numpy(h.view(np.int64).copy()), torch.from_numpy(o.view(np.int64).copy())
+            _, hv, ov = D.counts_buffer()   # even ranks: views of one buffer (the in-place path)
+            hv.copy_(torch.from_numpy(h.view(np.int64)))
+            ov.copy_(torch.from_numpy(o.view(np.int64)))
+            return hv, ov
 
         if perm is None:
             hist, ones = D.fused_stats_sharded(key, ctr0, n, local=local)
@@ -96,3 +101,15 @@ def test_allreduce_without_process_group_is_identity():
     o = torch.arange(32, dtype=torch.int64)
     h2, o2 = D.allreduce_counts(h.clone(), o.clone())
     assert torch.equal(h, h2) and torch.equal(o, o2)
+
+
+def test_counts_buffer_views():
+    """hist / ones from counts_buffer are recognised as one packed buffer (in-place exchange);
+    separate tensors or other views are not."""
+    from paper_2004_06278_b200 import dist as D
+    buf, h, o = D.counts_buffer()
+    assert buf.numel() == 65568 and h.numel() == 65536 and o.numel() == 32
+    p = D._packed(h, o)
+    assert p is not None and p.data_ptr() == buf.data_ptr() and p.numel() == 65568
+    assert D._packed(h, torch.zeros(32, dtype=torch.int64)) is None
+    assert D._packed(o, h) is None

@@ -270,6 +270,21 @@ def test_scaled_w64_equals_squares32():
     assert np.array_equal(got.astype(np.uint32), ref[:20000])
 
 
+def test_scaled_hand_values(golden_dir):
+    """Hand-derived W = 8 and W = 16 values (tests/golden/scaled_values.txt, each with its
+    derivation): pins the reduced-width masking, the W/2 rotation and the high-half
+    extraction below W = 64, where equality with squares32 does not reach."""
+    n = 0
+    with open(os.path.join(golden_dir, "scaled_values.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            W, ctr, key, want = line.split()
+            assert O.squares32_scaled(int(ctr, 16), int(key, 16), int(W)) == int(want, 16), line
+            n += 1
+    assert n == 8
+
+
 def test_scaled_key_zero_constant():
     assert all(O.squares32_scaled(c, 0, 16) == 0 for c in range(1 << 16))
 
@@ -322,3 +337,19 @@ def test_partition_examples_and_coverage():
             assert pos == n
     with pytest.raises(ValueError):
         O.partition(10, 0, 0)
+
+
+def test_xorfold_u32():
+    """oracle_xorfold_u32 (the CPU baseline's dead-code guard): XOR over i of
+    squares32(ctr0 + i) << (i mod 32).  Pinned by the hand value squares32(1, 2^32) = 0x2a
+    (n = 1), key 0 -> 0, n = 0 -> 0, and by the same fold of the per-element fill done in numpy
+    (a different loop: whole-array shifts and a reduction)."""
+    assert O.xorfold_u32(1 << 32, 1, 1) == 0x2A
+    assert O.xorfold_u32(0, 123, 1000) == 0
+    assert O.xorfold_u32(0x123456789ABCDEF3, 5, 0) == 0
+    key = int(O.keygen(1, 1)[0])
+    for ctr0, n in [(0, 1 << 16), ((1 << 64) - 100, 333), ((1 << 32) - 7, 64)]:
+        u = O.fill("u32", [key], ctr0, n)[0].astype(np.uint64)
+        sh = (np.arange(n, dtype=np.uint64) & np.uint64(31))
+        want = int(np.bitwise_xor.reduce(u << sh)) if n else 0
+        assert O.xorfold_u32(key, ctr0, n) == want
