@@ -60,7 +60,7 @@ class ClockSampler:
                0x20: "sync_boost", 0x1: "gpu_idle"}
 
     def __init__(self, torch_dev: int, interval_s: float = 0.005):
-        self.samples, self.reasons, self.ok = [], set(), False
+        self.samples, self.reasons, self.ok, self.power = [], set(), False, []
         self.interval = interval_s
         self._stop = threading.Event()
         try:
@@ -81,6 +81,10 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    self.power.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                except Exception:
+                    pass
                 try:
                     r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 except AttributeError:
@@ -106,8 +110,12 @@ class ClockSampler:
     def summary(self):
         if not self.ok:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": getattr(self, "err", "")}
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        out = {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+               "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if self.power:
+            out["power_w_median"] = statistics.median(self.power)
+            out["power_w_max"] = max(self.power)
+        return out
 
 
 # ------------------------------------------------------------------------------------- CPU oracle
@@ -118,10 +126,32 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (lscpu's "Model name"; /proc/cpuinfo on Linux)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:  # pragma: no cover
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _oracle_keys(w: SI.Workload, count: int):
+    """The workload's keys from the ORACLE's key utility (the reference arm and cpu_baseline
+    never load the product; tests/test_capi_host.py checks both key utilities agree)."""
+    import oracle as O
+    return [int(k) for k in O.keygen(w.key_seed, count)]
+
+
 def oracle_rate(w: SI.Workload, key: int, keys, budget_s: float, threads: int):
     """Times the oracle AS IT STANDS (oracle/oracle.c, gcc -O2, one loop per thread) on a
     bounded sample of workload w: `threads` disjoint contiguous shards of its counter range
-    (or key rows).  Returns (samples/s, samples, wall seconds, description)."""
+    (or key rows), each about `budget_s` seconds of one core.  Output buffers are allocated and
+    first touched, and the thread pool started, BEFORE the timed window (no page faults or
+    thread start-up inside it).  Returns (samples/s, samples, wall seconds, description)."""
     from concurrent.futures import ThreadPoolExecutor
 
     import numpy as np
@@ -149,22 +179,23 @@ def oracle_rate(w: SI.Workload, key: int, keys, budget_s: float, threads: int):
         kk = [np.array([key & M64], dtype=np.uint64) for _ in range(threads)]
         rows = 1
     bufs = [None] * threads
+    hs = [np.zeros(65536, np.uint64) for _ in range(threads)] if kind == "fused" else None
+    os_ = [np.zeros(32, np.uint64) for _ in range(threads)] if kind == "fused" else None
     if kind != "fused":
         dt = {"u32": np.uint32, "u64": np.uint64, "f32": np.float32}[kind]
-        bufs = [np.empty(per, dtype=dt) for _ in range(threads)]
+        bufs = [np.zeros(per, dtype=dt) for _ in range(threads)]   # zeros: pages touched now
     fn = None if kind == "fused" else getattr(lib, f"oracle_fill_{kind}")
 
     def work(i):
         if kind == "fused":
-            h = np.zeros(65536, np.uint64)
-            o = np.zeros(32, np.uint64)
-            lib.oracle_fused_stats(key & M64, (w.samples // threads) * i, per, h.ctypes.data, o.ctypes.data)
+            lib.oracle_fused_stats(key & M64, (w.samples // threads) * i, per, hs[i].ctypes.data, os_[i].ctypes.data)
         elif w.nkeys > 1:
             fn(kk[i].ctypes.data, rows, w.ctr0, w.n, bufs[i].ctypes.data, w.n)
         else:
             fn(kk[i].ctypes.data, 1, (w.samples // threads) * i, per, bufs[i].ctypes.data, per)
 
     with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda i: None, range(threads * 4)))   # start the workers outside the window
         t0 = time.perf_counter()
         list(ex.map(work, range(threads)))
         wall = time.perf_counter() - t0
@@ -176,9 +207,64 @@ def oracle_rate(w: SI.Workload, key: int, keys, budget_s: float, threads: int):
     return total / wall, total, wall, shape
 
 
-# ------------------------------------------------------------------------------------- GPU arm
-def run_ours(args, w: SI.Workload, rank: int, world: int, dev: int):
+def one_core_rates(key: int, window: int = 1 << 24, reps: int = 5) -> dict:
+    """the oracle on ONE core, a `window`-sample run per kind, median of
+    `reps`, in Msamples/s, each with a dead-code guard computed from its output after the timed
+    call (XOR-fold of the outputs; fused: the histogram total)."""
     import numpy as np
+
+    import oracle as O
+    lib = O.lib()
+    M64 = (1 << 64) - 1
+    kv = np.array([key & M64], dtype=np.uint64)
+    res = {}
+    for kind in ("u32", "u64", "f32", "fused", "u32_xorfold"):
+        ts, guard = [], 0
+        if kind in ("u32", "u64", "f32"):
+            buf = np.zeros(window, dtype={"u32": np.uint32, "u64": np.uint64, "f32": np.uint32}[kind])
+        for r in range(reps):
+            c0 = r * window
+            if kind == "fused":
+                h, o = np.zeros(65536, np.uint64), np.zeros(32, np.uint64)
+                t0 = time.perf_counter()
+                lib.oracle_fused_stats(key & M64, c0, window, h.ctypes.data, o.ctypes.data)
+                ts.append(time.perf_counter() - t0)
+                guard ^= int(h.sum()) ^ int(o[0])
+            elif kind == "u32_xorfold":
+                t0 = time.perf_counter()
+                g = lib.oracle_xorfold_u32(key & M64, c0, window)
+                ts.append(time.perf_counter() - t0)
+                guard ^= int(g)
+            else:
+                fn = getattr(lib, f"oracle_fill_{kind}")
+                t0 = time.perf_counter()
+                fn(kv.ctypes.data, 1, c0, window, buf.ctypes.data, window)
+                ts.append(time.perf_counter() - t0)
+                guard ^= int(np.bitwise_xor.reduce(buf.view(np.uint64 if kind == "u64" else np.uint32)))
+        res[kind] = {"msamples_per_s": window / statistics.median(ts) / 1e6, "guard": f"{guard:#x}"}
+    return {"window": window, "reps": reps, "statistic": "median", "rates": res,
+            "note": "one thread; u32/u64/f32 write a buffer (XOR of it printed as the guard), "
+                    "u32_xorfold writes nothing (its fold is the result), fused counts hist + ones"}
+
+
+def cpu_baseline_line(w: SI.Workload, budget_s: float, one_core: bool = True) -> dict:
+    """The cpu_baseline object (both arms build it with this function on the same workload)."""
+    cores = host_cores()
+    keys = _oracle_keys(w, min(w.nkeys, 64))
+    rate, samples, wall, shape = oracle_rate(w, keys[0], keys, budget_s, cores)
+    out = {"value": rate / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "cpu_model": cpu_model(),
+           "sample": f"{samples} samples of {w.name}: {shape}; {wall:.2f} s wall"}
+    if one_core:
+        out["one_core"] = one_core_rates(keys[0])
+    return out
+
+
+# ------------------------------------------------------------------------------------- GPU arm
+def run_ours(args, w: SI.Workload, rank: int, world: int, dev: int, entry: str = "auto"):
+    """Times `args.steps` steps of workload w on this rank.  entry: "auto" = the by-value
+    entry point sq_fill_*_k for single-key fills (key in the launch parameters), "devkeys" =
+    the 8(b) call sq_fill_* with a device key array."""
     import torch
     import torch.distributed as tdist
 
@@ -186,8 +272,8 @@ def run_ours(args, w: SI.Workload, rank: int, world: int, dev: int):
     from paper_2004_06278_b200 import dist as sqdist
 
     if args.scaling == "weak":
-        # weak scaling (per-GPU work fixed): rank r owns the r-th config-sized block of the
-        # counter space -- or the r-th block of nkeys keys -- so N GPUs do N batches.
+        # weak scaling (opt-in; per-GPU work fixed): rank r owns the r-th config-sized block of
+        # the counter space -- or the r-th block of nkeys keys -- so N GPUs do N batches.
         if w.shard == "key":
             keys_all = sq.keygen(w.key_seed, w.nkeys * world)
             k0, kn = rank * w.nkeys, w.nkeys
@@ -197,7 +283,8 @@ def run_ours(args, w: SI.Workload, rank: int, world: int, dev: int):
             k0, kn = 0, 1
             ctr0, n = (w.ctr0 + rank * w.n) & ((1 << 64) - 1), w.n
     else:
-        # strong scaling: the config's fixed total split into contiguous shards
+        # strong scaling (default; BASELINE.json's configs split a fixed total): the config's
+        # counters (c2, c3, c5) or key rows (c4) in contiguous shards
         keys_all = sq.keygen(w.key_seed, w.nkeys)
         if w.shard == "key":
             k0, kn = sqdist.key_shard(w.nkeys)
@@ -210,21 +297,21 @@ def run_ours(args, w: SI.Workload, rank: int, world: int, dev: int):
     samples_rank = kn * n
     stream = torch.cuda.current_stream(dev)
     if w.kind == "fused":
-        hist = torch.zeros(65536, dtype=torch.int64, device=dev)
-        ones = torch.zeros(32, dtype=torch.int64, device=dev)
+        # hist and ones are the two views of ONE packed buffer: zeroed by one memset, exchanged
+        # by one in-place all-reduce
+        buf, hist, ones = sqdist.counts_buffer(dev)
 
         def step():
             # one pass of the whole path over one batch: counts from zero,
-            # generate-and-reduce, and at N > 1 the one all-reduce of the counts (NCCL, same stream)
-            hist.zero_()
-            ones.zero_()
+            # generate-and-reduce, and at N > 1 the one all-reduce of the counts (same stream)
+            buf.zero_()
             sq.fused_stats(key0, ctr0, n, hist, ones, stream=stream)
             if world > 1:
                 sqdist.allreduce_counts(hist, ones)
     else:
         out = torch.empty((kn, n), dtype={"u32": torch.int32, "u64": torch.int64, "f32": torch.float32}[w.kind],
                           device=dev)
-        if kn == 1:
+        if kn == 1 and entry == "auto":
             # single key: the by-value entry point (sq_fill_*_k), key in the launch parameters
             fill_k = getattr(sq, f"fill_{w.kind}_k")
             out1 = out.view(-1)
@@ -242,45 +329,58 @@ def run_ours(args, w: SI.Workload, rank: int, world: int, dev: int):
     torch.cuda.synchronize(dev)
     if world > 1:
         tdist.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(dev) as clk:
         torch.cuda.synchronize(dev)
         if world > 1:
             tdist.barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
+        evs[0].record(stream)
+        for i in range(args.steps):
             step()
-        ev1.record(stream)
+            evs[i + 1].record(stream)
         torch.cuda.synchronize(dev)
         if world > 1:
             tdist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    ms = evs[0].elapsed_time(evs[-1])
+    per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    nb = min(20, args.steps)
+    burst_ms = sum(per_step[:nb]) / nb          # the first launches: before the power cap engages
+    t = torch.tensor([ms, burst_ms], dtype=torch.float64, device=dev)
     tot = torch.tensor([float(samples_rank)], dtype=torch.float64, device=dev)
     if world > 1:
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         tdist.all_reduce(tot, op=tdist.ReduceOp.SUM)
-    ms_max = float(t.item())
+    ms_max, burst_max = float(t[0].item()), float(t[1].item())
     total_samples = float(tot.item())
+    clocks = clk.summary()
     res = {
         "ms_total": ms_max,
         "ms_per_step": ms_max / args.steps,
         "value": total_samples * args.steps / (ms_max * 1e-3) / 1e9,
+        "burst": {"value": total_samples / (burst_max * 1e-3) / 1e9, "steps": nb,
+                  "ms_per_step": burst_max,
+                  "note": f"mean of the first {nb} timed steps (max over ranks); `value` is all {args.steps}"},
         "samples_per_step": int(total_samples),
         "samples_rank": samples_rank,
-        "clocks": clk.summary(),
+        "clocks": clocks,
         "key0": key0,
         "kn": kn,
     }
+    if world > 1:
+        allc = [None] * world
+        tdist.all_gather_object(allc, {"rank": rank, "sm_mhz": clocks.get("sm_mhz"), "reasons": clocks.get("reasons"),
+                                       "ms": ms, "samples": samples_rank})
+        res["per_rank"] = allc
     if w.kind == "fused" and world > 1:   # the exchange alone (it is also inside every timed step)
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        sqdist.allreduce_counts(hist, ones)
+        for _ in range(10):
+            sqdist.allreduce_counts(hist, ones)
         e1.record()
         torch.cuda.synchronize(dev)
-        res["allreduce_ms"] = e0.elapsed_time(e1)
-    # e2e through the C ABI with host buffers (rank-local shard; single-key workloads)
+        res["allreduce_ms"] = e0.elapsed_time(e1) / 10
+    # e2e through the C ABI with host buffers (rank-local shard)
     if not args.no_e2e:
         res["e2e"] = run_e2e(args, w, sq, key0, keys_d, ctr0, n, kn, dev, world)
     return res
@@ -291,17 +391,17 @@ def run_e2e(args, w, sq, key0, keys_d, ctr0, n, kn, dev, world):
     import torch.distributed as tdist
     steps = args.e2e_steps
     if w.kind == "fused":
-        host_h = torch.empty(65536 + 32, dtype=torch.int64).pin_memory()
-        hist = torch.zeros(65536, dtype=torch.int64, device=dev)
-        ones = torch.zeros(32, dtype=torch.int64, device=dev)
+        from paper_2004_06278_b200 import dist as sqdist
+        host = torch.empty(65536 + 32, dtype=torch.int64).pin_memory()
+        buf, hist, ones = sqdist.counts_buffer(dev)
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         for _ in range(steps):
-            hist.zero_()
-            ones.zero_()
+            buf.zero_()
             sq.fused_stats(key0, ctr0, n, hist, ones)
-            host_h[:65536].copy_(hist, non_blocking=True)
-            host_h[65536:].copy_(ones, non_blocking=True)
+            if world > 1:
+                sqdist.allreduce_counts(hist, ones)
+            host.copy_(buf, non_blocking=True)
             torch.cuda.synchronize(dev)
         wall = time.perf_counter() - t0
         d2h = (65536 + 32) * 8
@@ -328,7 +428,9 @@ def run_e2e(args, w, sq, key0, keys_d, ctr0, n, kn, dev, world):
         tdist.all_reduce(s, op=tdist.ReduceOp.SUM)
     return {"value": float(s.item()) * steps / float(t.item()) / 1e9, "unit": UNIT,
             "h2d_bytes_per_step": 8, "d2h_bytes_per_step": d2h, "steps": steps,
-            "note": "sq_fill_host / fused_stats + D2H of the counts; the 8-byte key travels in the launch parameters"}
+            "note": "sq_fill_host (chunked generate + D2H into pinned memory) / fused_stats (+ the all-reduce at "
+                    "N > 1) + D2H of the counts; host wall clock, max over ranks; the 8-byte key travels in the "
+                    "launch parameters"}
 
 
 def config_for(w: SI.Workload, world: int, scaling: str) -> dict:
@@ -347,9 +449,23 @@ def config_for(w: SI.Workload, world: int, scaling: str) -> dict:
         else "no HBM traffic (fused, counts only)"}
 
 
-def roofline_for(w: SI.Workload, res, peaks, peaks_src, prof):
+def sass_per_sample():
+    """SASS instructions and FMA-pipe slots per output sample of each hot loop of the LOADED
+    library (cuobjdump; tools/sass_counts.py), or {} if cuobjdump is unavailable."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import sass_counts
+        import paper_2004_06278_b200 as sq
+        return sass_counts.per_workload(sq.LIB_PATH)
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)[:200]}
+
+
+def roofline_for(w: SI.Workload, res, peaks, peaks_src, prof, sass=None, name=None):
     """Roofline of the dominant (only) kernel of the step."""
     ms_launch = res["ms_per_step"]
+    sass = sass or {}
+    name = name or w.name
     if w.kind == "fused":
         # ALU/FMA-bound: peak derived in DESIGN.md from the measured IMAD rate (64 lane-results
         # per clock per SM) and the 9 FMA-pipe slots squares32 needs per sample after the
@@ -359,8 +475,12 @@ def roofline_for(w: SI.Workload, res, peaks, peaks_src, prof):
         achieved = res["samples_rank"] / (ms_launch * 1e-3) / 1e9
         out = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gsamples/s",
                "frac": achieved / peak, "traffic": None,
-               "peak_note": "FMA-pipe floor 9 slots/sample (3 IMAD.WIDE x2 + 3 IMAD) at 64 slots/clk/SM, max SM clock"}
+               "peak_note": "FMA-pipe floor 9 slots/sample (3 IMAD.WIDE x2 + 3 IMAD) at 64 slots/clk/SM, max SM clock",
+               "frac_of_12_slot_ceiling": achieved / (64.0 / 12.0 * SM_PER_GPU * mhz * 1e-3),
+               "ceiling_12_slot_note": "SURVEY.md 8(d): 12 IMAD slots/sample (no finite-difference round 1)"}
         out.update(_pipes(prof, w.name, "fused_kernel"))
+        if name in sass:
+            out["sass"] = sass[name]
         return out
     bytes_launch = res["samples_rank"] * w.elem_bytes
     achieved = bytes_launch / (ms_launch * 1e-3) / 1e9
@@ -377,6 +497,8 @@ def roofline_for(w: SI.Workload, res, peaks, peaks_src, prof):
     out["other_peaks"] = {"spec_8000_GBps": achieved / 8000.0,
                           "memset_7354_GBps (profiles/r01_microbench_writes.json)": achieved / 7354.4,
                           "sm_store_6327_GBps (STG.256, same file)": achieved / 6326.5}
+    if name in sass:
+        out["sass"] = sass[name]
     return out
 
 
@@ -391,6 +513,9 @@ def _pipes(prof, name, kname):
                           "source": "profiles/ncu_summary.json (ncu --set full, same kernel)"}}
 
 
+DTYPE = {"u32": "u32", "u64": "u64", "f32": "u32->f32", "fused": "u32"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -399,11 +524,12 @@ def main():
     ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: every rank runs one config-sized batch of its own counter block")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default): the config's fixed total split over the ranks (BASELINE.json "
+                         "configs); weak: every rank runs one config-sized batch of its own counter block")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary c3/c4/c5 summary")
-    ap.add_argument("--cpu-budget", type=float, default=2.0, help="seconds per oracle thread (cpu_baseline)")
+    ap.add_argument("--cpu-budget", type=float, default=1.0, help="seconds per oracle thread (cpu_baseline)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -434,38 +560,47 @@ def main():
 
     res = run_ours(args, w, rank, world, local)
     extra = {}
+    sass = sass_per_sample() if rank == 0 else {}
     if not args.no_extra and args.workload == "c2":
         a2 = argparse.Namespace(**vars(args))
         a2.no_e2e = True
-        for name, steps in (("c3", 20), ("c4", 20), ("c5", 3)):
+        for name, wname, steps, entry in (("c2_devkeys", "c2", 50, "devkeys"), ("c3", "c3", 20, "auto"),
+                                          ("c4", "c4", 20, "auto"), ("c5", "c5", 3, "auto")):
             a2.steps, a2.warmup = steps, 3
-            ww = SI.CONFIGS[name]
-            r = run_ours(a2, ww, rank, world, local)
-            rl = roofline_for(ww, r, peaks, peaks_src, prof)
+            ww = SI.CONFIGS[wname]
+            r = run_ours(a2, ww, rank, world, local, entry=entry)
+            rl = roofline_for(ww, r, peaks, peaks_src, prof, sass, name)
             extra[name] = {"value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"], "steps": steps,
-                           "roofline": rl, "clocks": r["clocks"]}
+                           "roofline": rl, "clocks": r["clocks"], "gpu_launches": steps}
+            if name == "c2_devkeys":
+                extra[name]["entry"] = "sq_fill_u32 (device key array, SURVEY.md 8(b))"
             if "allreduce_ms" in r:
                 extra[name]["allreduce_ms"] = r["allreduce_ms"]
+            if "per_rank" in r:
+                extra[name]["per_rank"] = r["per_rank"]
 
     if rank == 0:
-        rl = roofline_for(w, res, peaks, peaks_src, prof)
-        cores = host_cores()
-        rate, samples, wall, shape = oracle_rate(w, res["key0"], sq.keygen(w.key_seed, min(w.nkeys, 64)).tolist(),
-                                                 args.cpu_budget, cores)
+        rl = roofline_for(w, res, peaks, peaks_src, prof, sass)
         line = {
             "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None,
-            "dtype": {"u32": "u32", "u64": "u64", "f32": "u32->f32", "fused": "u32"}[w.kind],
+            "dtype": DTYPE[w.kind],
             "data": "synthetic",
             "config": config_for(w, world, args.scaling),
             "roofline": rl,
-            "cpu_baseline": {"value": rate / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"{samples} samples of {w.name}: {shape}; {wall:.2f} s wall"},
+            "burst": res["burst"],
+            "cpu_baseline": cpu_baseline_line(w, args.cpu_budget, one_core=world == 1),
             "clocks": res["clocks"],
             "gpu_launches": args.steps,
             "impl": "ours",
+            "entry": "sq_fill_u32_k (key by value)" if w.kind != "fused" and w.nkeys == 1 else
+                     ("sq_fill_f32 (device keys)" if w.kind == "f32" else "sq_fused_stats"),
         }
+        if "per_rank" in res:
+            line["per_rank"] = res["per_rank"]
+        if "allreduce_ms" in res:
+            line["allreduce_ms"] = res["allreduce_ms"]
         if "e2e" in res:
             line["e2e"] = res["e2e"]
         if extra:
@@ -477,17 +612,17 @@ def main():
 
 
 def main_reference(args, w, rank, world):
-    """Reference arm: the CPU oracle as it stands on the host cores (rank 0 only)."""
+    """Reference arm: the CPU oracle as it stands on the host cores (rank 0 only).  Its keys come
+    from the oracle's own key utility: this process never loads the product library."""
     if rank != 0:
         return
-    import paper_2004_06278_b200 as sq  # only for the key (host function, no GPU work)
     import oracle as O
     O.build()
     cores = host_cores()
-    key0 = int(sq.keygen(w.key_seed, 1)[0]) & ((1 << 64) - 1)
-    keys = [int(k) & ((1 << 64) - 1) for k in sq.keygen(w.key_seed, min(w.nkeys, 64)).tolist()]
+    keys = _oracle_keys(w, min(w.nkeys, 64))
+    key0 = keys[0]
     # each step a bounded sample sized so that warmup + steps take <= ~120 s
-    per_step_budget = max(0.05, min(2.0, 120.0 / (args.steps + args.warmup)))
+    per_step_budget = max(0.05, min(args.cpu_budget, 120.0 / (args.steps + args.warmup)))
     for _ in range(args.warmup):
         oracle_rate(w, key0, keys, per_step_budget / 4, cores)
     tot_s, tot_n = 0.0, 0
@@ -501,11 +636,10 @@ def main_reference(args, w, rank, world):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3, "higher_is_better": True,
-        "scaling": args.scaling, "vs_baseline": None, "dtype": {"u32": "u32", "u64": "u64", "f32": "u32->f32",
-                                                               "fused": "u32"}[w.kind],
+        "scaling": args.scaling, "vs_baseline": None, "dtype": DTYPE[w.kind],
         "data": "synthetic", "impl": "reference",
         "config": config_for(w, world, args.scaling),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                          "sample": f"per step {last[0]} samples: {last[1]}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

@@ -86,8 +86,16 @@ struct WalkConst {
 #ifndef SQ_FUSED_PIPE
 #define SQ_FUSED_PIPE 1
 #endif
-#ifndef SQ_FUSED_FORM
-#define SQ_FUSED_FORM 0
+// Cross-term doubling form per round (squares_dev.cuh cross_add): rounds 2 and 3 double on the
+// IMAD pipe (form 0), round 4 with a funnel shift on the ALU (form 3), which moves one of the
+// FMA-heavy pipe's ~13.5 slots per sample to the ALU.  Measured on B200 (round 2, c5 at 2^34):
+// warp-specialised kernel 1084.6 (0/0/3) vs 1083.9 (0/3/0), 1077.2 (3/0/0), 1055.5 (0/0/0),
+// 1062.9 (0/1/3); lock-step kernel 1047.3 (0/0/3) vs 1041.4 (0/0/0); moving two or three
+// doublings loads the ALU pipe instead (994-1029).
+#ifndef SQ_FUSED_MIX2
+#define SQ_FUSED_MIX2 0
+#define SQ_FUSED_MIX3 0
+#define SQ_FUSED_MIX4 3
 #endif
 template <bool STRIDED, bool BITREV>
 __device__ __forceinline__ void gen8(State& s, const WalkConst& wc, uint32_t (&v)[8], uint32_t one) {
@@ -95,12 +103,7 @@ __device__ __forceinline__ void gen8(State& s, const WalkConst& wc, uint32_t (&v
 #pragma unroll
   for (int j = 0; j < 8; j++) {
     const uint64_t z = add64(y, wc.key);
-    // FORM 0 (plain doubling) measured fastest with the sweep scheme (991 vs 947 Gs/s FORM 1)
-#ifdef SQ_FUSED_MIX2
     const uint32_t o = squares32_mix<SQ_FUSED_MIX2, SQ_FUSED_MIX3, SQ_FUSED_MIX4>(y, z, u, one);
-#else
-    const uint32_t o = squares32_from<SQ_FUSED_FORM>(y, z, u, one);
-#endif
     v[j] = BITREV ? __brev(o) : o;
     y = STRIDED ? add64(y, wc.K) : z;
     u = j ? add64_3(u, s.e, wc.cst[j]) : add64(u, s.e);
@@ -178,11 +181,12 @@ __device__ __forceinline__ uint32_t epoch(State& s, const WalkConst& wc, uint32_
 // index).  Thread tid visits words tid, tid + T, ... (conflict-free banks).  Rare (the final
 // flush plus about one sweep per 2^29 samples per CTA), so it favours simplicity.  Called by
 // all threads between barriers (no concurrent ATOMS).
-__device__ __noinline__ void flush_bins(uint32_t* bins, unsigned long long* hist, unsigned long long* hi_cnt) {
+__device__ __noinline__ void flush_bins(uint32_t* bins, unsigned long long* hist, unsigned long long* hi_cnt,
+                                       uint32_t tid, uint32_t nthr) {
   uint32_t colcnt[16];
 #pragma unroll
   for (int j = 0; j < 16; j++) colcnt[j] = 0;
-  for (uint32_t w = threadIdx.x; w < 32768; w += blockDim.x) {
+  for (uint32_t w = tid; w < 32768; w += nthr) {
     const uint32_t wv = bins[w];
     if (!wv) continue;
     bins[w] = 0;
@@ -194,7 +198,7 @@ __device__ __noinline__ void flush_bins(uint32_t* bins, unsigned long long* hist
 #pragma unroll
     for (int j = 1; j < 16; j++) colcnt[j] += ((w >> (j - 1)) & 1u) ? (lo + hi) : 0u;
   }
-  // per thread <= 43 words x 0x1FFFE per flush: no 32-bit overflow before warp_flush16
+  // per thread <= 128 words (nthr >= 256) x 0x1FFFE per flush: no 32-bit overflow before warp_flush16
   warp_flush16(colcnt, hi_cnt);
 }
 
@@ -258,8 +262,8 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
     }
     if (++since_flush == kFlushEvery) {   // planes hold <= 63 per column: flush to the CTA totals
       since_flush = 0;
-#pragma unroll
       uint32_t colcnt[16] = {};   // transient: nothing column-wise lives across the loop
+#pragma unroll
       for (int p = 0; p < kPlanes; p++) { columns_add(colcnt, pl[p], 16u << p); pl[p] = 0; }
       warp_flush16(colcnt, lo_cnt);
     }
@@ -271,7 +275,7 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
     if (acc & kMask) hot_stamp[ep & 1] = ep + 1;
     __syncthreads();
     if (hot_stamp[ep & 1] == ep + 1) {
-      flush_bins(bins, hist, hi_cnt);
+      flush_bins(bins, hist, hi_cnt, tid, kFusedThreads);
       __syncthreads();
     }
   }
@@ -286,7 +290,7 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
   warp_flush16(colcnt, lo_cnt);
 
   // residual bins -> global hist (bits 16..31 derived from them)
-  flush_bins(bins, hist, hi_cnt);
+  flush_bins(bins, hist, hi_cnt, tid, kFusedThreads);
   __syncthreads();
   if (tid < 16) {
     const unsigned long long lo = lo_cnt[tid], hi = hi_cnt[tid];
@@ -295,10 +299,354 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
   }
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Warp-specialised variant (round 2).  The CTA's 32 warps split into kWsGen generator warps
+// and kWsRed reducer warps (the highest warp ids: the SMSP arbiter favours them, and they sit
+// on every sub-partition).  A generator warp walks its lanes' counter ranges exactly like the
+// kernel above (gen8), counts bits 0..15 with the same carry-save tree, and hands each
+// 8-sample batch (1 KiB per warp) to its reducer through a shared-memory ring of kWsDepth
+// slots guarded by mbarriers (full: 32 producer arrivals, empty: 32 consumer arrivals).  A
+// reducer warp serves kWsGen / kWsRed generator warps round-robin and owns the histogram
+// updates (ATOMS + sweep vote).  The sweep scheme's epoch barrier (hist16.cuh) is a named
+// barrier among the reducers only, so the generators never stop at a barrier and the
+// FMA-heavy generation and the ALU/LSU-heavy reduction run side by side on every SMSP
+// instead of in lock-step phases.
+// 1: warp-specialised kernel (default, measured faster); 0: the lock-step kernel above.
+#ifndef SQ_FUSED_IMPL
+#define SQ_FUSED_IMPL 1
+#endif
+#ifndef SQ_WS_GEN
+#define SQ_WS_GEN 24
+#endif
+#ifndef SQ_WS_RED_FIRST
+#define SQ_WS_RED_FIRST 0
+#endif
+#ifndef SQ_WS_MAXNREG
+#define SQ_WS_MAXNREG 0     // e.g. 72 for the generators (then SQ_WS_REDNREG = 40 for the reducers)
+#endif
+#ifndef SQ_WS_REDNREG
+#define SQ_WS_REDNREG 40
+#endif
+#ifndef SQ_WS_DEPTH
+#define SQ_WS_DEPTH 1
+#endif
+#ifndef SQ_WS_EPOCH_STEPS
+#define SQ_WS_EPOCH_STEPS 2
+#endif
+constexpr int kWsThreads = 1024;
+constexpr int kWsGen = SQ_WS_GEN;                       // generator warps
+constexpr int kWsRed = 32 - kWsGen;                     // reducer warps
+constexpr int kWsPer = kWsGen / kWsRed;                 // generator warps per reducer warp
+constexpr int kWsDepth = SQ_WS_DEPTH;                   // ring slots per generator warp
+constexpr int kWsEpochSteps = SQ_WS_EPOCH_STEPS;        // reducer steps (kWsPer slots each) per epoch
+#ifndef SQ_WS_SLOT_BATCHES
+#define SQ_WS_SLOT_BATCHES 4
+#endif
+constexpr int kWsSB = SQ_WS_SLOT_BATCHES;               // batches (8 samples per lane) per ring slot
+constexpr int kWsSlotWords = 256 * kWsSB;
+static_assert(kWsSB == 1 || kWsSB == 2 || kWsSB == 4, "a slot holds 1, 2 or 4 batches (divides a 4-batch tree)");
+constexpr uint32_t kWsEpochIncs = (uint32_t)kWsRed * 32 * kWsPer * 8 * kWsSB * kWsEpochSteps;
+constexpr uint32_t kWsT = sweep_threshold(kWsEpochIncs);
+constexpr uint32_t kWsMask = sweep_mask(kWsT);
+static_assert(kWsGen % kWsRed == 0, "each reducer serves a whole number of generator warps");
+static_assert(kWsT >= 0x100 && kWsT + kWsEpochIncs <= 0xFFFFu, "epoch bound of the sweep scheme (reducers)");
+constexpr size_t kWsRingBytes = (size_t)kWsGen * kWsDepth * kWsSlotWords * 4;
+constexpr size_t kWsBarOff = 32768 * 4 + kWsRingBytes;
+constexpr size_t kWsSmem = kWsBarOff + (size_t)kWsGen * kWsDepth * 2 * 8 + 16 * 8 + 16 * 8 + 2 * 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// Reducer-side wait: try the phase once, then back off with nanosleep between polls so that a
+// waiting reducer warp does not take issue slots from the generators (the FMA-bound side).
+#ifndef SQ_WS_SLEEP_NS
+#define SQ_WS_SLEEP_NS 0
+#endif
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+  while (!ok) {
+    if (SQ_WS_SLEEP_NS) __nanosleep(SQ_WS_SLEEP_NS);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+
+// Generator: one 32-sample Harley-Seal tree = 4 batches = 2 ring slots; each batch is stored
+// as soon as it is generated.  MASKED: samples past this lane's count are zeroed for the bit
+// counting (the reducer masks them in the histogram).  Slot layout: 4 rows of 32 lanes x
+// uint4 (row = batch half), so every STS.128 / LDS.128 covers 512 contiguous bytes.
+template <bool MASKED, bool STRIDED, bool BITREV>
+__device__ __forceinline__ uint32_t ws_gen_tree(State& s, const WalkConst& wc, uint32_t one, uint32_t* ring_g,
+                                                uint64_t* full_g, uint64_t* empty_g, uint32_t b0, int64_t rem,
+                                                uint32_t lane, uint32_t& ones, uint32_t& twos, uint32_t& fours,
+                                                uint32_t& eights) {
+  uint32_t eightsAB[2], foursAB[2];
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    uint32_t v[8];
+    gen8<STRIDED, BITREV>(s, wc, v, one);
+    const uint32_t b = b0 + k, sl = b / kWsSB, sub = b % kWsSB, slot = sl % kWsDepth, round = sl / kWsDepth;
+    if (sub == 0 && round) mbar_wait_sleep(&empty_g[slot], (round - 1) & 1);
+    uint4* dst = (uint4*)(ring_g + slot * kWsSlotWords) + sub * 64;
+    dst[lane] = make_uint4(v[0], v[1], v[2], v[3]);
+    dst[32 + lane] = make_uint4(v[4], v[5], v[6], v[7]);
+    if (sub == kWsSB - 1) mbar_arrive(&full_g[slot]);
+    uint32_t w[4], twosA, twosB;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      uint32_t a = v[2 * i], c = v[2 * i + 1];
+      if (MASKED) {
+        if (!(rem - 8 * k > 2 * i)) a = 0;
+        if (!(rem - 8 * k > 2 * i + 1)) c = 0;
+      }
+      w[i] = __byte_perm(a, c, 0x5410);
+    }
+    const int blk = k >> 1, h = k & 1;
+    csa(twosA, ones, ones, w[0], w[1]);
+    csa(twosB, ones, ones, w[2], w[3]);
+    csa(foursAB[h], twos, twos, twosA, twosB);
+    if (h) csa(eightsAB[blk], fours, fours, foursAB[0], foursAB[1]);
+  }
+  uint32_t sixteens;
+  csa(sixteens, eights, eights, eightsAB[0], eightsAB[1]);
+  return sixteens;
+}
+
+// Histogram update for the reducers: the increment (v & 0x10000) | one as ONE LOP3 (`one` = 1
+// in a register ptxas cannot see through; with two immediates it takes two).
+__device__ __forceinline__ uint32_t ws_hist_add(uint32_t* bins, uint32_t v, uint32_t one, bool valid = true) {
+  uint32_t inc;
+  asm("lop3.b32 %0, %1, 0x10000, %2, 0xEA;" : "=r"(inc) : "r"(v), "r"(one));   // (a & b) | c
+  if (!valid) inc = 0;
+  return atomicAdd(&bins[v >> 17], inc);
+}
+
+// Reducer: one slot (kWsSB batches = 8 kWsSB samples per lane) of a generator warp.
+template <bool MASKED>
+__device__ __forceinline__ void ws_consume(const uint32_t* ring_g, uint64_t* full_g, uint64_t* empty_g, uint32_t sl,
+                                           uint32_t lane, uint32_t* bins, uint32_t& acc, int64_t valid,
+                                           uint32_t one) {
+  const uint32_t slot = sl % kWsDepth, round = sl / kWsDepth;
+  mbar_wait_sleep(&full_g[slot], round & 1);
+  const uint4* src = (const uint4*)(ring_g + slot * kWsSlotWords);
+  uint32_t v[8 * kWsSB];
+#pragma unroll
+  for (int r = 0; r < 2 * kWsSB; r++) {
+    const uint4 p = src[32 * r + lane];
+    v[4 * r] = p.x; v[4 * r + 1] = p.y; v[4 * r + 2] = p.z; v[4 * r + 3] = p.w;
+  }
+  mbar_arrive(&empty_g[slot]);
+#pragma unroll
+  for (int i = 0; i < 8 * kWsSB; i += 2) {
+    if (MASKED)
+      acc |= ws_hist_add(bins, v[i], one, valid > i) | ws_hist_add(bins, v[i + 1], one, valid > i + 1);
+    else
+      acc |= ws_hist_add(bins, v[i], one) | ws_hist_add(bins, v[i + 1], one);
+  }
+}
+
+// nb: batches per generator lane (a multiple of 4, the same for every lane of the grid);
+// nfull: batches in which every lane of the grid has 8 valid samples.
+template <bool STRIDED, bool BITREV>
+__global__ void __launch_bounds__(kWsThreads, 1)
+fused_ws_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t r, uint32_t nb, uint32_t nfull,
+                unsigned long long* __restrict__ hist, unsigned long long* __restrict__ ones_out, uint32_t one) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  uint32_t* bins = smem;
+  uint32_t* ring = smem + 32768;
+  uint64_t* full = (uint64_t*)((char*)smem + kWsBarOff);
+  uint64_t* empty = full + kWsGen * kWsDepth;
+  unsigned long long* lo_cnt = (unsigned long long*)(empty + kWsGen * kWsDepth);
+  unsigned long long* hi_cnt = lo_cnt + 16;
+  volatile uint32_t* hot_stamp = (volatile uint32_t*)(hi_cnt + 16);
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  // broadcast from lane 0 so that ptxas treats the role branch as warp-uniform (it then keeps
+  // the walk constants in uniform registers inside it)
+  const uint32_t warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  for (uint32_t i = tid; i < 32768; i += kWsThreads) bins[i] = 0;
+  if (tid < 16) { lo_cnt[tid] = 0; hi_cnt[tid] = 0; }
+  if (tid < 2) hot_stamp[tid] = 0;
+  if (tid < kWsGen * kWsDepth) { mbar_init(&full[tid], 32); mbar_init(&empty[tid], 32); }
+  // per-key walk constants, computed in convergent code from kernel parameters (uniform
+  // registers; inside the role branch ptxas rematerialises them with IMAD.WIDE)
+  const uint64_t K = STRIDED ? stride * key : key;
+  WalkConst wc;
+  {
+    const uint64_t k2x2 = 2 * K * K;
+    wc.key = key;
+    wc.K = K;
+    wc.cst[0] = 0;
+#pragma unroll
+    for (int j = 1; j < 8; j++) wc.cst[j] = wc.cst[j - 1] + k2x2;
+    wc.cst8 = wc.cst[7] + k2x2;
+  }
+  __syncthreads();
+
+  // role: generator warps gw = 0..kWsGen-1, reducer warps rw = 0..kWsRed-1.  SQ_WS_RED_FIRST
+  // puts the reducers on the LOWEST warp ids (the SMSP arbiter favours high ids)
+#if SQ_WS_RED_FIRST
+  const bool is_gen = warp >= kWsRed;
+  const uint32_t gw = warp - kWsRed, rw_ = warp;
+#else
+  const bool is_gen = warp < kWsGen;
+  const uint32_t gw = warp, rw_ = warp - kWsGen;
+#endif
+  if (is_gen) {
+    // ------------------------------------------------------------------ generator warp
+#if SQ_WS_MAXNREG
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(SQ_WS_MAXNREG));
+#endif
+    const uint64_t t = (uint64_t)blockIdx.x * (kWsGen * 32) + gw * 32 + lane;
+    const uint64_t start = t * q + (t < r ? t : r);
+    const uint64_t cnt = q + (t < r ? 1 : 0);
+    State st = STRIDED ? state_at_strided(ctr0 + start * stride, key, K) : state_at(ctr0 + start, key);
+    uint32_t* ring_g = ring + gw * kWsDepth * kWsSlotWords;
+    uint64_t* full_g = full + gw * kWsDepth;
+    uint64_t* empty_g = empty + gw * kWsDepth;
+    uint32_t ones = 0, twos = 0, fours = 0, eights = 0;
+    uint32_t pl[kPlanes];
+#pragma unroll
+    for (int p = 0; p < kPlanes; p++) pl[p] = 0;
+    int since_flush = 0;
+    for (uint32_t b = 0; b < nb; b += 4) {
+      uint32_t sixteens;
+      if (b + 4 <= nfull) {
+        sixteens = ws_gen_tree<false, STRIDED, BITREV>(st, wc, one, ring_g, full_g, empty_g, b, 32, lane, ones, twos,
+                                                       fours, eights);
+      } else {
+        const int64_t rem = 8 * (uint64_t)b < cnt ? (int64_t)(cnt - 8 * (uint64_t)b) : 0;
+        sixteens = ws_gen_tree<true, STRIDED, BITREV>(st, wc, one, ring_g, full_g, empty_g, b, rem, lane, ones, twos,
+                                                      fours, eights);
+      }
+      uint32_t c = sixteens;
+#pragma unroll
+      for (int p = 0; p < kPlanes; p++) {
+        const uint32_t tt = pl[p] & c;
+        pl[p] ^= c;
+        c = tt;
+      }
+      if (++since_flush == 63) {   // planes hold <= 63 per column
+        since_flush = 0;
+        uint32_t colcnt[16] = {};
+#pragma unroll
+        for (int p = 0; p < kPlanes; p++) { columns_add(colcnt, pl[p], 16u << p); pl[p] = 0; }
+        warp_flush16(colcnt, lo_cnt);
+      }
+    }
+    uint32_t colcnt[16] = {};
+    columns_add(colcnt, ones, 1);
+    columns_add(colcnt, twos, 2);
+    columns_add(colcnt, fours, 4);
+    columns_add(colcnt, eights, 8);
+#pragma unroll
+    for (int p = 0; p < kPlanes; p++) columns_add(colcnt, pl[p], 16u << p);
+    warp_flush16(colcnt, lo_cnt);
+  } else {
+    // ------------------------------------------------------------------ reducer warp
+#if SQ_WS_MAXNREG
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(SQ_WS_REDNREG));
+#endif
+    const uint32_t rw = rw_, rtid = rw_ * 32 + lane;
+    int64_t cnt_g[kWsPer];
+#pragma unroll
+    for (int j = 0; j < kWsPer; j++) {
+      const uint64_t t = (uint64_t)blockIdx.x * (kWsGen * 32) + (rw * kWsPer + j) * 32 + lane;
+      cnt_g[j] = (int64_t)(q + (t < r ? 1 : 0));
+    }
+    // slots: nb / kWsSB per generator warp; slot sl holds batches kWsSB*sl .. kWsSB*sl + kWsSB-1
+    const uint32_t ns = nb / kWsSB, nsfull = nfull / kWsSB;
+    uint32_t ep = 0;
+    for (uint32_t sl = 0; sl < ns; ep++) {
+      uint32_t acc = 0;
+      const uint32_t se = (sl + kWsEpochSteps < ns) ? sl + kWsEpochSteps : ns;
+      for (; sl < se; sl++) {
+        if (sl < nsfull) {
+#pragma unroll
+          for (int j = 0; j < kWsPer; j++) {
+            const uint32_t g = rw * kWsPer + j;
+            ws_consume<false>(ring + g * kWsDepth * kWsSlotWords, full + g * kWsDepth, empty + g * kWsDepth, sl, lane,
+                              bins, acc, 8 * kWsSB, one);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < kWsPer; j++) {
+            const uint32_t g = rw * kWsPer + j;
+            ws_consume<true>(ring + g * kWsDepth * kWsSlotWords, full + g * kWsDepth, empty + g * kWsDepth, sl, lane,
+                             bins, acc, cnt_g[j] - 8 * kWsSB * (int64_t)sl, one);
+          }
+        }
+      }
+      // epoch boundary among the reducers (named barrier 1): vote, sweep if any word got hot
+      if (acc & kWsMask) hot_stamp[ep & 1] = ep + 1;
+      asm volatile("bar.sync 1, %0;" ::"n"(kWsRed * 32) : "memory");
+      if (hot_stamp[ep & 1] == ep + 1) {
+        flush_bins(bins, hist, hi_cnt, rtid, kWsRed * 32);
+        asm volatile("bar.sync 1, %0;" ::"n"(kWsRed * 32) : "memory");
+      }
+    }
+    flush_bins(bins, hist, hi_cnt, rtid, kWsRed * 32);
+  }
+  __syncthreads();
+  if (tid < 16) {
+    const unsigned long long lo = lo_cnt[tid], hi = hi_cnt[tid];
+    if (lo) atomicAdd(&ones_out[tid], lo);
+    if (hi) atomicAdd(&ones_out[16 + tid], hi);
+  }
+}
+
+static int launch_fused_ws(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
+                           uint64_t* hist, uint64_t* ones, cudaStream_t stream, const DeviceInfo* di) {
+  const bool strided = stride != 1, bitrev = (flags & SQ_FUSED_BITREV) != 0;
+  decltype(&fused_ws_kernel<false, false>) kern =
+      strided ? (bitrev ? fused_ws_kernel<true, true> : fused_ws_kernel<true, false>)
+              : (bitrev ? fused_ws_kernel<false, true> : fused_ws_kernel<false, false>);
+  static std::atomic<bool> attr_set[kMaxDevices][4];
+  std::atomic<bool>& as = attr_set[di->device][(strided ? 2 : 0) + (bitrev ? 1 : 0)];
+  if (!as.load(std::memory_order_acquire)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWsSmem);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    as.store(true, std::memory_order_release);
+  }
+  uint64_t blocks = (n + (1ull << 20) - 1) >> 20;
+  if (blocks > (uint64_t)di->sms) blocks = di->sms;
+  if (blocks < 1) blocks = 1;
+  const uint64_t T = blocks * (kWsGen * 32);
+  const uint64_t q = n / T, r = n % T;
+  const uint64_t per = q + (r ? 1 : 0);
+  const uint64_t nb = ((per + 31) / 32) * 4;      // batches per lane, whole 4-batch trees
+  if (nb > 0xFFFFFFF0ull) return SQ_ERANGE;
+  const uint64_t nfull = q / 8;
+  kern<<<(unsigned)blocks, kWsThreads, kWsSmem, stream>>>(key, ctr0, stride, q, r, (uint32_t)nb,
+                                                          (uint32_t)(nfull < nb ? nfull : nb),
+                                                          (unsigned long long*)hist, (unsigned long long*)ones, 1u);
+  return set_cuda_error(cudaGetLastError());
+}
+
 int launch_fused(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
                  uint64_t* hist, uint64_t* ones, cudaStream_t stream) {
   const DeviceInfo* di = device_info();
   if (!di) return SQ_ECUDA;
+  if (SQ_FUSED_IMPL == 1) return launch_fused_ws(key, ctr0, stride, n, flags, hist, ones, stream, di);
   const bool strided = stride != 1, bitrev = (flags & SQ_FUSED_BITREV) != 0;
   decltype(&fused_kernel<false, false>) kern =
       strided ? (bitrev ? fused_kernel<true, true> : fused_kernel<true, false>)
