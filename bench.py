@@ -478,7 +478,8 @@ def roofline_for(w: SI.Workload, res, peaks, peaks_src, prof, sass=None, name=No
                "peak_note": "FMA-pipe floor 9 slots/sample (3 IMAD.WIDE x2 + 3 IMAD) at 64 slots/clk/SM, max SM clock",
                "frac_of_12_slot_ceiling": achieved / (64.0 / 12.0 * SM_PER_GPU * mhz * 1e-3),
                "ceiling_12_slot_note": "SURVEY.md 8(d): 12 IMAD slots/sample (no finite-difference round 1)"}
-        out.update(_pipes(prof, w.name, "fused_kernel"))
+        out.update(_pipes(prof, w.name, prof.get(w.name, {}).get("kernel", "fused_ws_kernel")
+                          if str(prof.get(w.name, {}).get("kernel", "")).startswith("fused") else "fused_ws_kernel"))
         if name in sass:
             out["sass"] = sass[name]
         return out
@@ -510,6 +511,9 @@ def _pipes(prof, name, kname):
         return {}
     return {"pipes_ncu": {"fmaheavy_pct": p.get("fmaheavy_pct"), "alu_pct": p.get("alu_pct"),
                           "issue_pct": p.get("issue_active_pct"),
+                          "inst_executed_per_sample": p.get("inst_executed_per_sample"),
+                          "fmaheavy_inst_per_sample": p.get("inst_fmaheavy_per_sample"),
+                          "alu_inst_per_sample": p.get("inst_alu_per_sample"),
                           "source": "profiles/ncu_summary.json (ncu --set full, same kernel)"}}
 
 

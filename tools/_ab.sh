@@ -1,3 +1,1 @@
-for r in 1 2; do
-for v in sb4_003 sb4_030 sb4_000 sb4_300 sb4_003rf sb4_003e1 sb4_003nr sb4_013; do SQ_LIB=exp/v/$v.so python tools/c5time.py $v; done
-done
+python tools/burst_ab.py exp/v/old.so exp/v/mb2.so exp/v/mb3.so exp/v/mb4.so

@@ -32,6 +32,9 @@ KEYS = {
     "smem_atom_bank_conflicts": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum",
     "inst_executed": "smsp__inst_executed.sum",
     "sm_clock_hz": "sm__cycles_elapsed.avg.per_second",
+    "inst_fmaheavy": "smsp__inst_executed_pipe_fmaheavy.sum",
+    "inst_alu": "smsp__inst_executed_pipe_alu.sum",
+    "inst_lsu": "smsp__inst_executed_pipe_lsu.sum",
 }
 UNIT_SCALE = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1, "usecond": 1e3, "msecond": 1e6,
               "nsecond": 1, "ns": 1, "us": 1e3, "ms": 1e6, "GHz": 1e9, "MHz": 1e6, "Hz": 1, "hz": 1}
@@ -79,14 +82,29 @@ def main():
         kname = s["kernel"]
         import re
         m = re.search(r"fill_kernel<\(?(?:int\))?\s*(\d)", kname)
-        s["kernel"] = "fused_kernel" if "fused" in kname else (f"fill_kernel<{m.group(1)}>" if m else kname)
+        s["kernel"] = ("fused_ws_kernel" if "fused_ws" in kname else "fused_kernel") if "fused" in kname else \
+            (f"fill_kernel<{m.group(1)}>" if m else kname)
         s["kernel_full"] = kname
         s["source"] = f"profiles/{tag}_ncu_{cfg}_raw.csv (ncu --set full --clock-control none)"
+        # executed instructions per output sample (warp instructions x 32 / samples of the launch;
+        # tools/profile_all.sh launches c2 2^30, c3 2^29, c4 2^30, c5 2^34 samples)
+        ns = {"c2": 1 << 30, "c3": 1 << 29, "c4": 1 << 30, "c5": 1 << 34}[cfg]
+        for k in ("inst_executed", "inst_fmaheavy", "inst_alu", "inst_lsu"):
+            if isinstance(s.get(k), float):
+                s[k + "_per_sample"] = s[k] * 32 / ns
         summary[cfg] = s
-    lpath = os.path.join(OUT, f"{tag}_launches.csv")
+    for suffix, key in (("", "launch_list"), ("_c5", "launch_list_c5")):
+        launch_list(tag, suffix, key, summary)
+    with open(os.path.join(PROF, "ncu_summary.json"), "w") as f:
+        json.dump(summary, f, indent=1)
+    print(json.dumps(summary, indent=1))
+
+
+def launch_list(tag, suffix, key, summary):
+    lpath = os.path.join(OUT, f"{tag}_launches{suffix}.csv")
     if os.path.exists(lpath):
         txt = open(lpath).read()
-        with open(os.path.join(PROF, f"{tag}_launches.csv"), "w") as f:
+        with open(os.path.join(PROF, f"{tag}_launches{suffix}.csv"), "w") as f:
             f.write(txt)
         lines = [l for l in txt.splitlines() if l.startswith('"')]
         rows = list(csv.reader(io.StringIO("\n".join(lines))))
@@ -96,17 +114,17 @@ def main():
         for r in rows[1:]:
             t = float(r[vi].replace(",", ""))
             tot += t
-            name = "fill_kernel" if "fill_kernel" in r[ki] else ("fused_kernel" if "fused" in r[ki] else r[ki][:60])
+            name = "fill_kernel" if "fill_kernel" in r[ki] else \
+                (("fused_ws_kernel" if "fused_ws" in r[ki] else "fused_kernel") if "fused" in r[ki] else r[ki][:60])
             per.setdefault(name, [0, 0.0])
             per[name][0] += 1
             per[name][1] += t
-        summary["launch_list"] = {
-            "source": f"profiles/{tag}_launches.csv (ncu --metrics gpu__time_duration.sum --clock-control none; bench.py --steps 5 --warmup 3)",
+        cmd = "bench.py --steps 5 --warmup 3 --no-e2e --no-extra" if not suffix else \
+            "bench.py --workload c5 --steps 2 --warmup 3 --no-e2e --no-extra"
+        summary[key] = {
+            "source": f"profiles/{tag}_launches{suffix}.csv (ncu --metrics gpu__time_duration.sum --clock-control none; {cmd})",
             "kernels": {k: {"launches": v[0], "total_ns": v[1], "share": v[1] / tot} for k, v in per.items()},
         }
-    with open(os.path.join(PROF, "ncu_summary.json"), "w") as f:
-        json.dump(summary, f, indent=1)
-    print(json.dumps(summary, indent=1))
 
 
 if __name__ == "__main__":
