@@ -77,6 +77,7 @@ __device__ __forceinline__ uint64_t add64_3(uint64_t a, uint64_t b, uint64_t c) 
 //                                               dependency chain (shorter latency per round)
 //   3  IMAD(xl, SHF(RZ:xh, 1), hi)           -- the doubling as a funnel shift with an immediate
 //                                               amount: ALU pipe, one register read
+//   6  hi + ((xl * xh) << 1)                 -- product first, doubling and add after it (LEA)
 // Measured on B200: form 3 is fastest for the library's 32-bit fills (the ALU has room next to
 // the stores), form 0 for compute-only loops (fused statistics, Stream): the default here.
 #ifndef SQ_ROUND_FORM
@@ -85,6 +86,14 @@ __device__ __forceinline__ uint64_t add64_3(uint64_t a, uint64_t b, uint64_t c) 
 template <int FORM = SQ_ROUND_FORM>
 __device__ __forceinline__ uint32_t cross_add(uint32_t xl, uint32_t xh, uint32_t hi, uint32_t one) {
   if (FORM == 0) return mad_lo(xl, xh << 1, hi);
+  if (FORM == 6) {
+    // hi + ((xl * xh) << 1): the product without the doubling (IMAD with no addend, off the
+    // chain through the IMAD.WIDE), then shift-and-add; ptxas emits LEA / IMAD-by-2 forms here
+    uint32_t p, r;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(p) : "r"(xl), "r"(xh));
+    asm("shl.b32 %0, %1, 1;\n\tadd.u32 %0, %0, %2;" : "=r"(r) : "r"(p), "r"(hi));
+    return r;
+  }
   uint32_t d;
   if (FORM == 3) {
     asm("shf.l.clamp.b32 %0, 0, %1, 1;" : "=r"(d) : "r"(xh));

@@ -86,7 +86,7 @@ template <int KIND, int FORM, int NW>
 __device__ __forceinline__ void put(uint32_t (&v)[NW], int j, uint64_t y, uint64_t z, uint64_t u, uint32_t one) {
   if (KIND == KIND_U32 || KIND == KIND_F32) {
 #ifdef SQ_FILL_MIX2
-    const uint32_t o = (KIND == KIND_U32) ? squares32_mix<SQ_FILL_MIX2, SQ_FILL_MIX3, SQ_FILL_MIX4>(y, z, u, one) : squares32_from<FORM>(y, z, u, one);
+    const uint32_t o = squares32_mix<SQ_FILL_MIX2, SQ_FILL_MIX3, SQ_FILL_MIX4>(y, z, u, one);
 #else
     const uint32_t o = squares32_from<FORM>(y, z, u, one);
 #endif

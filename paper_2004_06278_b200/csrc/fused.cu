@@ -86,15 +86,15 @@ struct WalkConst {
 #ifndef SQ_FUSED_PIPE
 #define SQ_FUSED_PIPE 1
 #endif
-// Cross-term doubling form per round (squares_dev.cuh cross_add): rounds 2 and 3 double on the
-// IMAD pipe (form 0), round 4 with a funnel shift on the ALU (form 3), which moves one of the
-// FMA-heavy pipe's ~13.5 slots per sample to the ALU.  Measured on B200 (round 2, c5 at 2^34):
-// warp-specialised kernel 1084.6 (0/0/3) vs 1083.9 (0/3/0), 1077.2 (3/0/0), 1055.5 (0/0/0),
-// 1062.9 (0/1/3); lock-step kernel 1047.3 (0/0/3) vs 1041.4 (0/0/0); moving two or three
-// doublings loads the ALU pipe instead (994-1029).
+// Cross-term form per round (squares_dev.cuh cross_add): rounds 2 and 3 as form 6 (the
+// product xl*xh first, off the chain through the IMAD.WIDE, then doubled and added), round 4 as
+// form 3 (funnel-shift doubling on the ALU).  Measured on B200 (round 2, c5 at 2^34,
+// warp-specialised kernel): 6/6/3 1117.6 Gsamples/s; 6/6/1 1112.7; 6/0/3 1097.6;
+// 6/6/6 1092; 0/6/3 1090; 0/0/3 1084.6; 0/3/0 1083.9; 6/6/0 1077.5; 3/0/0 1077.2; 3/6/3 1057;
+// 0/0/0 1055.5; the lock-step kernel with 6/6/3: 1057.8.
 #ifndef SQ_FUSED_MIX2
-#define SQ_FUSED_MIX2 0
-#define SQ_FUSED_MIX3 0
+#define SQ_FUSED_MIX2 6
+#define SQ_FUSED_MIX3 6
 #define SQ_FUSED_MIX4 3
 #endif
 template <bool STRIDED, bool BITREV>

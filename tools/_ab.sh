@@ -1,3 +1,1 @@
-python bench.py > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.err; echo rc=$?
-sleep 20
-python bench.py --no-e2e > gpurun_out/r02_bench_rep2.json 2>/dev/null; echo rc=$?
+for r in 1 2; do for v in m663 m660 m666 m663L m661 m663rf m663nr m363; do SQ_LIB=exp/v/$v.so python tools/c5time.py $v; done; done
