@@ -175,6 +175,7 @@ int sq_fill_keyctr(int kind, const uint64_t* keys_dev, uint64_t nkeys, uint64_t 
  *   ones_dev[j] += #{i : (u_i >> j) & 1 == 1}        j < 32, j = 0 the least significant bit
  * into caller-initialised device arrays (uint64).  No sample is stored.  Accumulation makes
  * chunked and sharded runs compose by addition.  hist_dev and ones_dev must be 8-byte aligned.
+ * Any n < 2^64 (runs above 2^48 samples are split into several launches internally).
  * Returns SQ_OK without launching when n == 0.  Errors: SQ_EINVAL (NULL / misaligned),
  * SQ_ECUDA (launch failure).
  * -------------------------------------------------------------------------------------- */

@@ -642,11 +642,11 @@ static int launch_fused_ws(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_
   return set_cuda_error(cudaGetLastError());
 }
 
-int launch_fused(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
-                 uint64_t* hist, uint64_t* ones, cudaStream_t stream) {
-  const DeviceInfo* di = device_info();
-  if (!di) return SQ_ECUDA;
-  if (SQ_FUSED_IMPL == 1) return launch_fused_ws(key, ctr0, stride, n, flags, hist, ones, stream, di);
+static int launch_fused_one(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
+                            uint64_t* hist, uint64_t* ones, cudaStream_t stream, const DeviceInfo* di) {
+#if SQ_FUSED_IMPL == 1
+  return launch_fused_ws(key, ctr0, stride, n, flags, hist, ones, stream, di);
+#else
   const bool strided = stride != 1, bitrev = (flags & SQ_FUSED_BITREV) != 0;
   decltype(&fused_kernel<false, false>) kern =
       strided ? (bitrev ? fused_kernel<true, true> : fused_kernel<true, false>)
@@ -671,6 +671,24 @@ int launch_fused(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint3
   kern<<<(unsigned)blocks, kFusedThreads, kFusedSmem, stream>>>(
       key, ctr0, stride, q, r, (uint32_t)epochs, (unsigned long long*)hist, (unsigned long long*)ones, 1u);
   return set_cuda_error(cudaGetLastError());
+#endif
+}
+
+// Any n < 2^64: launches of at most 2^48 samples (the per-launch batch counters are 32-bit),
+// accumulating into the same counts; counters continue mod 2^64 across the pieces.
+int launch_fused(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t n, uint32_t flags,
+                 uint64_t* hist, uint64_t* ones, cudaStream_t stream) {
+  const DeviceInfo* di = device_info();
+  if (!di) return SQ_ECUDA;
+  constexpr uint64_t kPiece = 1ull << 48;
+  while (n) {
+    const uint64_t m = n < kPiece ? n : kPiece;
+    const int rc = launch_fused_one(key, ctr0, stride, m, flags, hist, ones, stream, di);
+    if (rc != SQ_OK) return rc;
+    ctr0 += m * stride;
+    n -= m;
+  }
+  return SQ_OK;
 }
 
 }  // namespace sq
