@@ -334,9 +334,13 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
 #ifndef SQ_WS_EPOCH_STEPS
 #define SQ_WS_EPOCH_STEPS 2
 #endif
-constexpr int kWsThreads = 1024;
+#ifndef SQ_WS_RED
+#define SQ_WS_RED (32 - SQ_WS_GEN)
+#endif
 constexpr int kWsGen = SQ_WS_GEN;                       // generator warps
-constexpr int kWsRed = 32 - kWsGen;                     // reducer warps
+constexpr int kWsRed = SQ_WS_RED;                       // reducer warps
+constexpr int kWsThreads = 32 * (kWsGen + kWsRed);
+static_assert(kWsThreads <= 1024, "one CTA of at most 32 warps");
 constexpr int kWsPer = kWsGen / kWsRed;                 // generator warps per reducer warp
 constexpr int kWsDepth = SQ_WS_DEPTH;                   // ring slots per generator warp
 constexpr int kWsEpochSteps = SQ_WS_EPOCH_STEPS;        // reducer steps (kWsPer slots each) per epoch
