@@ -301,14 +301,14 @@ fused_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64_t 
 
 
 // ---------------------------------------------------------------------------------------
-// Warp-specialised variant (round 2).  The CTA's 32 warps split into kWsGen generator warps
-// and kWsRed reducer warps (the highest warp ids: the SMSP arbiter favours them, and they sit
-// on every sub-partition).  A generator warp walks its lanes' counter ranges exactly like the
-// kernel above (gen8), counts bits 0..15 with the same carry-save tree, and hands each
-// 8-sample batch (1 KiB per warp) to its reducer through a shared-memory ring of kWsDepth
-// slots guarded by mbarriers (full: 32 producer arrivals, empty: 32 consumer arrivals).  A
-// reducer warp serves kWsGen / kWsRed generator warps round-robin and owns the histogram
-// updates (ATOMS + sweep vote).  The sweep scheme's epoch barrier (hist16.cuh) is a named
+// Warp-specialised variant (round 2, the default c5 kernel).  The CTA's 32
+// warps split into kWsGen = 24 generator warps and kWsRed = 8 reducer warps (the highest warp
+// ids: the SMSP arbiter favours them, and they sit on every sub-partition).  A generator warp
+// walks its lanes' counter ranges exactly like the kernel above (gen8), counts bits 0..15
+// with the same carry-save tree, and hands each 32-sample tree (4 batches, 4 KiB per warp) to
+// its reducer through a shared-memory ring of kWsDepth slots guarded by mbarriers (full: 32
+// producer arrivals, empty: 32 consumer arrivals).  A reducer warp serves kWsGen / kWsRed
+// generator warps round-robin and owns the histogram updates (ATOMS + sweep vote).  The sweep scheme's epoch barrier (hist16.cuh) is a named
 // barrier among the reducers only, so the generators never stop at a barrier and the
 // FMA-heavy generation and the ALU/LSU-heavy reduction run side by side on every SMSP
 // instead of in lock-step phases.
@@ -368,8 +368,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
-// Reducer-side wait: try the phase once, then back off with nanosleep between polls so that a
-// waiting reducer warp does not take issue slots from the generators (the FMA-bound side).
+// Ring wait (both sides): one try_wait per pass (measured faster than a try_wait/branch spin
+// loop: 1081 vs 1072 Gsamples/s); SQ_WS_SLEEP_NS > 0 adds a nanosleep back-off between polls
+// (measured no better).
 #ifndef SQ_WS_SLEEP_NS
 #define SQ_WS_SLEEP_NS 0
 #endif
@@ -387,18 +388,10 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
         "selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
   }
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)), "r"(parity) : "memory");
-}
-
-// Generator: one 32-sample Harley-Seal tree = 4 batches = 2 ring slots; each batch is stored
-// as soon as it is generated.  MASKED: samples past this lane's count are zeroed for the bit
-// counting (the reducer masks them in the histogram).  Slot layout: 4 rows of 32 lanes x
-// uint4 (row = batch half), so every STS.128 / LDS.128 covers 512 contiguous bytes.
+// Generator: one 32-sample Harley-Seal tree = 4 batches = 4 / kWsSB ring slots; each batch is
+// stored as soon as it is generated.  MASKED: samples past this lane's count are zeroed for
+// the bit counting (the reducer masks them in the histogram).  Slot layout: 2 kWsSB rows of 32
+// lanes x uint4 (row = batch half), so every STS.128 / LDS.128 covers 512 contiguous bytes.
 template <bool MASKED, bool STRIDED, bool BITREV>
 __device__ __forceinline__ uint32_t ws_gen_tree(State& s, const WalkConst& wc, uint32_t one, uint32_t* ring_g,
                                                 uint64_t* full_g, uint64_t* empty_g, uint32_t b0, int64_t rem,
