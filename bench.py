@@ -433,6 +433,7 @@ def run_e2e(args, w, sq, key0, keys_d, ctr0, n, kn, dev, world):
         tdist.all_reduce(s, op=tdist.ReduceOp.SUM)
     return {"value": float(s.item()) * steps / float(t.item()) / 1e9, "unit": UNIT,
             "h2d_bytes_per_step": 8, "d2h_bytes_per_step": d2h, "steps": steps,
+            "d2h_GBps": d2h * steps / float(t.item()) / 1e9 if world == 1 else None,
             "note": "sq_fill_host (chunked generate + D2H into pinned memory) / fused_stats (+ the all-reduce at "
                     "N > 1) + D2H of the counts; host wall clock, max over ranks; the 8-byte key travels in the "
                     "launch parameters"}
