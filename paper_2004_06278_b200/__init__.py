@@ -328,7 +328,16 @@ def fill_keyctr(kind: str, keys: torch.Tensor, ctr: int, out: torch.Tensor | Non
     return out
 
 
-def _counts_pair(hist, ones, device):
+def _zeros(shape, dev, stream):
+    """Zeroed int64 counts, the memset enqueued on `stream` (the stream the kernel will run on)
+    so that it is ordered before the accumulating kernel even when `stream` is not current."""
+    if stream is None:
+        return torch.zeros(shape, dtype=torch.int64, device=dev)
+    with torch.cuda.stream(stream):
+        return torch.zeros(shape, dtype=torch.int64, device=dev)
+
+
+def _counts_pair(hist, ones, device, stream=None):
     """(hist, ones, device): allocated zeroed on `device` when None, else validated."""
     dev = None
     if hist is not None:
@@ -340,9 +349,9 @@ def _counts_pair(hist, ones, device):
     elif device is not None and _device(device) != dev:
         raise ValueError(f"counts are on {dev}, device={device}")
     if hist is None:
-        hist = torch.zeros(HIST_BINS, dtype=torch.int64, device=dev)
+        hist = _zeros(HIST_BINS, dev, stream)
     if ones is None:
-        ones = torch.zeros(32, dtype=torch.int64, device=dev)
+        ones = _zeros(32, dev, stream)
     return hist, ones, dev
 
 
@@ -350,7 +359,7 @@ def fused_stats_ex(key: int, ctr0: int, n: int, stride: int = 1, bitrev: bool = 
                    hist: torch.Tensor | None = None, ones: torch.Tensor | None = None, device=None, stream=None):
     """Fused statistics over counters ctr0 + i*stride, optionally of bit-reversed outputs."""
     n = _count(n)
-    hist, ones, dev = _counts_pair(hist, ones, device)
+    hist, ones, dev = _counts_pair(hist, ones, device, stream)
     with torch.cuda.device(dev):
         _check("sq_fused_stats_ex", _load().sq_fused_stats_ex(_u64(key), _u64(ctr0), _u64(stride), n,
                                                               SQ_FUSED_BITREV if bitrev else 0, hist.data_ptr(),
@@ -364,7 +373,7 @@ def transitions(key: int, ctr0: int, n: int, stride: int = 1, bitrev: bool = Fal
     n = _count(n)
     if count is None:
         dev = _device(device)
-        count = torch.zeros(1, dtype=torch.int64, device=dev)
+        count = _zeros(1, dev, stream)
     else:
         dev = _check_counts(count, 1, "count", _device(device) if device is not None else None)
     with torch.cuda.device(dev):
@@ -381,7 +390,7 @@ def scaled_hist(W: int, keys: torch.Tensor, hist: torch.Tensor | None = None, st
         raise ValueError("W must be an even integer in [8, 32]")
     nb = 1 << (W // 2)
     if hist is None:
-        hist = torch.zeros((keys.numel(), nb), dtype=torch.int64, device=dev)
+        hist = _zeros((keys.numel(), nb), dev, stream)
     else:
         _check_counts(hist, keys.numel() * nb, "hist", dev)
     with torch.cuda.device(dev):
@@ -395,7 +404,7 @@ def fused_stats(key: int, ctr0: int, n: int, hist: torch.Tensor | None = None,
     """Accumulate the top-16-bit histogram (65536 bins) and the 32 per-bit ones counts of
     squares32 over [ctr0, ctr0 + n) into int64 CUDA tensors (allocated zeroed if None)."""
     n = _count(n)
-    hist, ones, dev = _counts_pair(hist, ones, device)
+    hist, ones, dev = _counts_pair(hist, ones, device, stream)
     with torch.cuda.device(dev):
         _check("sq_fused_stats", _load().sq_fused_stats(_u64(key), _u64(ctr0), n, hist.data_ptr(),
                                                         ones.data_ptr(), _stream_handle(stream, dev)))
