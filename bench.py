@@ -488,6 +488,7 @@ def roofline_for(w: SI.Workload, res, peaks, peaks_src, prof, sass=None, name=No
                           if str(prof.get(w.name, {}).get("kernel", "")).startswith("fused") else "fused_ws_kernel"))
         if name in sass:
             out["sass"] = sass[name]
+            out["imad_issue"] = _imad_issue(achieved, sass[name], mhz, 3)
         return out
     bytes_launch = res["samples_rank"] * w.elem_bytes
     achieved = bytes_launch / (ms_launch * 1e-3) / 1e9
@@ -506,7 +507,23 @@ def roofline_for(w: SI.Workload, res, peaks, peaks_src, prof, sass=None, name=No
                           "sm_store_6327_GBps (STG.256, same file)": achieved / 6326.5}
     if name in sass:
         out["sass"] = sass[name]
+        out["imad_issue"] = _imad_issue(res["samples_rank"] / (ms_launch * 1e-3) / 1e9, sass[name],
+                                        peaks.get("sm_max_mhz", 1965.0), 4 if w.kind == "u64" else 3)
     return out
+
+
+def _imad_issue(gsps, sass, mhz, wide):
+    """SURVEY.md 8(d)'s "% IMAD peak": samples/s x FMA-heavy slots per sample (from the SASS of
+    the hot loop) / (SMs x 64 lane-slots per clock x clock), with IMAD.WIDE/HI weighted 2 (their
+    issue cost) and 2.5 (their measured cost in dependent chains); `wide` = WIDE/HI
+    instructions per sample."""
+    slots = sass.get("fma_slots_per_sample")
+    if slots is None:
+        return None
+    cap = SM_PER_GPU * 64 * mhz * 1e6   # wide: IMAD.WIDE/HI per sample (3 squares32, 4 squares64)
+    return {"fma_slots_per_sample": slots, "frac_wide_2": gsps * 1e9 * slots / cap,
+            "frac_wide_2p5": gsps * 1e9 * (slots + 0.5 * wide) / cap,
+            "note": "achieved x SASS FMA-heavy slots / (148 SMs x 64 x max SM clock)"}
 
 
 def _pipes(prof, name, kname):
