@@ -357,7 +357,20 @@ static_assert(kWsGen % kWsRed == 0, "each reducer serves a whole number of gener
 static_assert(kWsT >= 0x100 && kWsT + kWsEpochIncs <= 0xFFFFu, "epoch bound of the sweep scheme (reducers)");
 constexpr size_t kWsRingBytes = (size_t)kWsGen * kWsDepth * kWsSlotWords * 4;
 constexpr size_t kWsBarOff = 32768 * 4 + kWsRingBytes;
-constexpr size_t kWsSmem = kWsBarOff + (size_t)kWsGen * kWsDepth * 2 * 8 + 16 * 8 + 16 * 8 + 2 * 4;
+// SQ_DEBUG_RING builds (tests only: SQ_LIB=<debug build>) tag every ring slot with its sequence
+// number and trap on any out-of-order hand-off -- a protocol check in lieu of compute-sanitizer's
+// racecheck, which is closed on this pool.  SQ_DEBUG_RING_BREAK (negative control)
+// drops one of the generators' waits on the empty barrier, which the check must catch.
+#ifdef SQ_DEBUG_RING
+constexpr size_t kWsTagBytes = (size_t)kWsGen * kWsDepth * 4;
+#define SQ_RING_TAG_ARG , volatile uint32_t* tag_g
+#define SQ_RING_TAG_PASS(x) , (x)
+#else
+constexpr size_t kWsTagBytes = 0;
+#define SQ_RING_TAG_ARG
+#define SQ_RING_TAG_PASS(x)
+#endif
+constexpr size_t kWsSmem = kWsBarOff + (size_t)kWsGen * kWsDepth * 2 * 8 + 16 * 8 + 16 * 8 + 2 * 4 + kWsTagBytes;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -396,17 +409,37 @@ template <bool MASKED, bool STRIDED, bool BITREV>
 __device__ __forceinline__ uint32_t ws_gen_tree(State& s, const WalkConst& wc, uint32_t one, uint32_t* ring_g,
                                                 uint64_t* full_g, uint64_t* empty_g, uint32_t b0, int64_t rem,
                                                 uint32_t lane, uint32_t& ones, uint32_t& twos, uint32_t& fours,
-                                                uint32_t& eights) {
+                                                uint32_t& eights SQ_RING_TAG_ARG) {
   uint32_t eightsAB[2], foursAB[2];
 #pragma unroll
   for (int k = 0; k < 4; k++) {
     uint32_t v[8];
     gen8<STRIDED, BITREV>(s, wc, v, one);
     const uint32_t b = b0 + k, sl = b / kWsSB, sub = b % kWsSB, slot = sl % kWsDepth, round = sl / kWsDepth;
+#ifndef SQ_DEBUG_RING_BREAK
     if (sub == 0 && round) mbar_wait_sleep(&empty_g[slot], (round - 1) & 1);
+#else
+    // negative control: skip the wait of round 1 only (the barrier phases stay consistent, so
+    // nothing can hang; slot 0 may be rewritten while its reducer still reads round 0)
+    if (sub == 0 && round > 1) mbar_wait_sleep(&empty_g[slot], (round - 1) & 1);
+#endif
+#ifdef SQ_DEBUG_RING
+    if (sub == 0) {   // slot being rewritten: invalidate its tag first
+      __syncwarp();
+      if (lane == 0) tag_g[slot] = 0;
+      __syncwarp();
+    }
+#endif
     uint4* dst = (uint4*)(ring_g + slot * kWsSlotWords) + sub * 64;
     dst[lane] = make_uint4(v[0], v[1], v[2], v[3]);
     dst[32 + lane] = make_uint4(v[4], v[5], v[6], v[7]);
+#ifdef SQ_DEBUG_RING
+    if (sub == kWsSB - 1) {
+      __syncwarp();
+      if (lane == 0) tag_g[slot] = sl + 1;
+      __syncwarp();
+    }
+#endif
     if (sub == kWsSB - 1) mbar_arrive(&full_g[slot]);
     uint32_t w[4], twosA, twosB;
 #pragma unroll
@@ -442,9 +475,12 @@ __device__ __forceinline__ uint32_t ws_hist_add(uint32_t* bins, uint32_t v, uint
 template <bool MASKED>
 __device__ __forceinline__ void ws_consume(const uint32_t* ring_g, uint64_t* full_g, uint64_t* empty_g, uint32_t sl,
                                            uint32_t lane, uint32_t* bins, uint32_t& acc, int64_t valid,
-                                           uint32_t one) {
+                                           uint32_t one SQ_RING_TAG_ARG) {
   const uint32_t slot = sl % kWsDepth, round = sl / kWsDepth;
   mbar_wait_sleep(&full_g[slot], round & 1);
+#ifdef SQ_DEBUG_RING
+  if (tag_g[slot] != sl + 1) __trap();   // handed over before it was written
+#endif
   const uint4* src = (const uint4*)(ring_g + slot * kWsSlotWords);
   uint32_t v[8 * kWsSB];
 #pragma unroll
@@ -452,6 +488,10 @@ __device__ __forceinline__ void ws_consume(const uint32_t* ring_g, uint64_t* ful
     const uint4 p = src[32 * r + lane];
     v[4 * r] = p.x; v[4 * r + 1] = p.y; v[4 * r + 2] = p.z; v[4 * r + 3] = p.w;
   }
+#ifdef SQ_DEBUG_RING
+  __syncwarp();
+  if (tag_g[slot] != sl + 1) __trap();   // overwritten while being read
+#endif
   mbar_arrive(&empty_g[slot]);
 #pragma unroll
   for (int i = 0; i < 8 * kWsSB; i += 2) {
@@ -476,6 +516,10 @@ fused_ws_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64
   unsigned long long* lo_cnt = (unsigned long long*)(empty + kWsGen * kWsDepth);
   unsigned long long* hi_cnt = lo_cnt + 16;
   volatile uint32_t* hot_stamp = (volatile uint32_t*)(hi_cnt + 16);
+#ifdef SQ_DEBUG_RING
+  volatile uint32_t* tags = (volatile uint32_t*)(hot_stamp + 2);
+  for (uint32_t i = threadIdx.x; i < kWsGen * kWsDepth; i += blockDim.x) tags[i] = 0;
+#endif
   const uint32_t tid = threadIdx.x, lane = tid & 31;
   // broadcast from lane 0 so that ptxas treats the role branch as warp-uniform (it then keeps
   // the walk constants in uniform registers inside it)
@@ -529,11 +573,11 @@ fused_ws_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64
       uint32_t sixteens;
       if (b + 4 <= nfull) {
         sixteens = ws_gen_tree<false, STRIDED, BITREV>(st, wc, one, ring_g, full_g, empty_g, b, 32, lane, ones, twos,
-                                                       fours, eights);
+                                                       fours, eights SQ_RING_TAG_PASS(tags + gw * kWsDepth));
       } else {
         const int64_t rem = 8 * (uint64_t)b < cnt ? (int64_t)(cnt - 8 * (uint64_t)b) : 0;
         sixteens = ws_gen_tree<true, STRIDED, BITREV>(st, wc, one, ring_g, full_g, empty_g, b, rem, lane, ones, twos,
-                                                      fours, eights);
+                                                      fours, eights SQ_RING_TAG_PASS(tags + gw * kWsDepth));
       }
       uint32_t c = sixteens;
 #pragma unroll
@@ -582,14 +626,14 @@ fused_ws_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64
           for (int j = 0; j < kWsPer; j++) {
             const uint32_t g = rw * kWsPer + j;
             ws_consume<false>(ring + g * kWsDepth * kWsSlotWords, full + g * kWsDepth, empty + g * kWsDepth, sl, lane,
-                              bins, acc, 8 * kWsSB, one);
+                              bins, acc, 8 * kWsSB, one SQ_RING_TAG_PASS(tags + g * kWsDepth));
           }
         } else {
 #pragma unroll
           for (int j = 0; j < kWsPer; j++) {
             const uint32_t g = rw * kWsPer + j;
             ws_consume<true>(ring + g * kWsDepth * kWsSlotWords, full + g * kWsDepth, empty + g * kWsDepth, sl, lane,
-                             bins, acc, cnt_g[j] - 8 * kWsSB * (int64_t)sl, one);
+                             bins, acc, cnt_g[j] - 8 * kWsSB * (int64_t)sl, one SQ_RING_TAG_PASS(tags + g * kWsDepth));
           }
         }
       }
