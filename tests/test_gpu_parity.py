@@ -357,3 +357,26 @@ def test_fill_host_chunking(sq, kind, scratch_bytes, n, ctr0):
         got = host.numpy()[: n * es].view(want.dtype)
         assert np.array_equal(got, want), (kind, pinned, first_mismatch(got, want))
         assert (host.numpy()[n * es:] == 0).all()
+
+
+def test_parity_harness_detects_a_flipped_word(sq):
+    """Negative test (failure detection): the comparison used throughout this file
+    must fail, and name the first bad index, when one output word or one count is wrong."""
+    key = int(O.keygen(1, 1)[0])
+    n = (1 << 16) + 3
+    out = sq.fill_u32_k(key, 0, n)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(np.uint32).copy()
+    want = O.fill("u32", [key], 0, n)[0]
+    assert np.array_equal(got, want)
+    for i in (0, 12345, n - 1):
+        bad = got.copy()
+        bad[i] ^= np.uint32(1 << (i % 32))
+        assert not np.array_equal(bad, want)
+        assert first_mismatch(bad, want).startswith(f"1 mismatches; first at {i}:")
+    h, o = _fused(sq, key, 0, n)
+    hw, ow = O.fused_stats(key, 0, n)
+    assert np.array_equal(h, hw) and np.array_equal(o, ow)
+    h2 = h.copy()
+    h2[int(np.argmax(h2))] += np.uint64(1)
+    assert not np.array_equal(h2, hw)
