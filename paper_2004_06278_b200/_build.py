@@ -14,7 +14,7 @@ LIB = os.path.join(PKG, "libsquares.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["capi.cu", "fill.cu", "fused.cu", "keyctr.cu", "scaled.cu", "keygen.cpp"]
-HEADERS = ["squares_device.cuh", "sq_internal.h", "hist16.cuh"]
+HEADERS = ["sq_internal.h", "hist16.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v"]
 

@@ -9,14 +9,14 @@
 // row starts m elements before the row (m = row misalignment), and elements outside [0, n)
 // are masked (head, ragged tail).  The flattened (row, chunk) space is split into one
 // contiguous range per warp of a persistent grid (#SM x occupancy CTAs), balanced to within
-// one chunk.  A lane walks its chunks with the multiply-free jump of squares_device.cuh
+// one chunk.  A lane walks its chunks with the multiply-free jump of include/squares_dev.cuh
 // (J = 32*SPL counters) and its SPL consecutive counters with the Weyl step.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <atomic>
 
-#include "squares_device.cuh"
+#include "../../include/squares_dev.cuh"
 #include "sq_internal.h"
 
 namespace sq {
@@ -41,7 +41,7 @@ __device__ __forceinline__ void st256(void* p, const uint32_t* v) {
                : "memory");
 }
 
-// Per-row constants of the counter walk (squares_device.cuh): the key, the stepping
+// Per-row constants of the counter walk (include/squares_dev.cuh): the key, the stepping
 // increment K = stride*key, the chunk jump (J*K, J(J-1)K^2, 2JK^2) and cst[j] = j*2K^2 for
 // the in-chunk 3-input u step.
 template <int SPL>

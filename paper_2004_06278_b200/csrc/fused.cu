@@ -5,7 +5,7 @@
 //
 // Design:
 //  * One CTA of 1024 threads per SM (persistent), each thread owning one contiguous counter
-//    range, walked with the multiply-free Weyl/finite-difference step (squares_device.cuh).
+//    range, walked with the multiply-free Weyl/finite-difference step (include/squares_dev.cuh).
 //  * hist: a 65536-bin histogram held in shared memory as 16-bit counters packed two per
 //    32-bit word (128 KiB; 32-bit bins would need 256 KiB > 227 KiB): word w holds
 //    A = count(2w) + count(2w+1) and B = count(2w+1).  Exact by the sweep scheme of
@@ -27,7 +27,7 @@
 #include <atomic>
 
 #include "hist16.cuh"
-#include "squares_device.cuh"
+#include "../../include/squares_dev.cuh"
 #include "sq_internal.h"
 
 namespace sq {
@@ -80,7 +80,7 @@ struct WalkConst {
 };
 
 // 8 consecutive samples from state s; s advances by 8 counters.  u uses the 3-input step
-// u(c+j+1) = u(c+j) + e(c) + j*2k^2 (squares_device.cuh), e advances once per group.
+// u(c+j+1) = u(c+j) + e(c) + j*2k^2 (include/squares_dev.cuh), e advances once per group.
 // STRIDED: counters advance by `stride` (y by K, z = y + key separately); BITREV: each
 // output is bit-reversed before it is counted ("bits-reversed tests").
 #ifndef SQ_FUSED_PIPE

@@ -7,7 +7,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include "squares_device.cuh"
+#include "../../include/squares_dev.cuh"
 #include "sq_internal.h"
 
 namespace sq {
