@@ -139,6 +139,9 @@ def per_workload(lib: str = LIB) -> dict:
                       "fma_slots_per_sample": round(v["fma_slots_per_sample"], 4),
                       "multiply_instructions_per_sample": round(v["multiply_instructions_per_sample"], 4),
                       "alu_per_sample": round(v["alu_per_sample"], 4),
+                      "mix_per_sample": {op: round(c / (32 if k.startswith("c5") else
+                                                        (8 if k == "c3" else 16)), 4)
+                                         for op, c in v["mix"].items()},
                       "loop": desc, "symbol": v["symbol"]}
     return res
 
