@@ -344,6 +344,11 @@ static_assert(kWsThreads <= 1024, "one CTA of at most 32 warps");
 constexpr int kWsPer = kWsGen / kWsRed;                 // generator warps per reducer warp
 constexpr int kWsDepth = SQ_WS_DEPTH;                   // ring slots per generator warp
 constexpr int kWsEpochSteps = SQ_WS_EPOCH_STEPS;        // reducer steps (kWsPer slots each) per epoch
+// Two carry-save trees per generator iteration, folded by one more level into a weight-32 word
+// (one plane ripple per 64 samples instead of per 32): 1115 -> 1135 Gsamples/s.
+#ifndef SQ_WS_TREE2
+#define SQ_WS_TREE2 1
+#endif
 #ifndef SQ_WS_SLOT_BATCHES
 #define SQ_WS_SLOT_BATCHES 4
 #endif
@@ -569,6 +574,45 @@ fused_ws_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64
 #pragma unroll
     for (int p = 0; p < kPlanes; p++) pl[p] = 0;
     int since_flush = 0;
+#if SQ_WS_TREE2
+    // two 32-sample trees per iteration, their weight-16 words folded into a weight-32 word by
+    // one more carry-save level: one ripple into the planes per 64 samples
+    uint32_t sx = 0;   // weight-16 carry-save state
+    for (uint32_t b = 0; b < nb; b += 8) {
+      uint32_t s16[2];
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const uint32_t bb = b + 4 * h;
+        if (bb + 4 <= nfull) {
+          s16[h] = ws_gen_tree<false, STRIDED, BITREV>(st, wc, one, ring_g, full_g, empty_g, bb, 32, lane, ones,
+                                                       twos, fours, eights SQ_RING_TAG_PASS(tags + gw * kWsDepth));
+        } else {
+          const int64_t rem = 8 * (uint64_t)bb < cnt ? (int64_t)(cnt - 8 * (uint64_t)bb) : 0;
+          s16[h] = ws_gen_tree<true, STRIDED, BITREV>(st, wc, one, ring_g, full_g, empty_g, bb, rem, lane, ones,
+                                                      twos, fours, eights SQ_RING_TAG_PASS(tags + gw * kWsDepth));
+        }
+      }
+      uint32_t c;
+      csa(c, sx, sx, s16[0], s16[1]);
+#pragma unroll
+      for (int p = 0; p < kPlanes; p++) {
+        const uint32_t tt = pl[p] & c;
+        pl[p] ^= c;
+        c = tt;
+      }
+      if (++since_flush == 63) {   // planes hold <= 63 per column
+        since_flush = 0;
+        uint32_t colcnt[16] = {};
+#pragma unroll
+        for (int p = 0; p < kPlanes; p++) { columns_add(colcnt, pl[p], 32u << p); pl[p] = 0; }
+        warp_flush16(colcnt, lo_cnt);
+      }
+    }
+    uint32_t colcnt[16] = {};
+    columns_add(colcnt, sx, 16);
+#pragma unroll
+    for (int p = 0; p < kPlanes; p++) { columns_add(colcnt, pl[p], 32u << p); pl[p] = 0; }
+#else
     for (uint32_t b = 0; b < nb; b += 4) {
       uint32_t sixteens;
       if (b + 4 <= nfull) {
@@ -595,12 +639,13 @@ fused_ws_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64
       }
     }
     uint32_t colcnt[16] = {};
+#pragma unroll
+    for (int p = 0; p < kPlanes; p++) columns_add(colcnt, pl[p], 16u << p);
+#endif
     columns_add(colcnt, ones, 1);
     columns_add(colcnt, twos, 2);
     columns_add(colcnt, fours, 4);
     columns_add(colcnt, eights, 8);
-#pragma unroll
-    for (int p = 0; p < kPlanes; p++) columns_add(colcnt, pl[p], 16u << p);
     warp_flush16(colcnt, lo_cnt);
   } else {
     // ------------------------------------------------------------------ reducer warp
@@ -674,7 +719,8 @@ static int launch_fused_ws(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_
   const uint64_t T = blocks * (kWsGen * 32);
   const uint64_t q = n / T, r = n % T;
   const uint64_t per = q + (r ? 1 : 0);
-  const uint64_t nb = ((per + 31) / 32) * 4;      // batches per lane, whole 4-batch trees
+  // batches per lane, whole 4-batch trees (pairs of trees with SQ_WS_TREE2)
+  const uint64_t nb = SQ_WS_TREE2 ? ((per + 63) / 64) * 8 : ((per + 31) / 32) * 4;
   if (nb > 0xFFFFFFF0ull) return SQ_ERANGE;
   const uint64_t nfull = q / 8;
   kern<<<(unsigned)blocks, kWsThreads, kWsSmem, stream>>>(key, ctr0, stride, q, r, (uint32_t)nb,

@@ -106,8 +106,14 @@ def counts(lib: str = LIB) -> dict:
         sts = [i for i, (_, s) in enumerate(ins) if opcode(s) == "STS.128"]
         if len(sts) < 8:
             continue
-        g0 = max(i for i in range(sts[0]) if opcode(ins[i][1]).startswith("BRA.U"))
         g1 = next(i for i in range(sts[7], len(ins)) if opcode(ins[i][1]) == "BRA")
+
+        def target(txt):
+            m = re.search(r"0x([0-9a-f]+)\s*$", txt)
+            return int(m.group(1), 16) if m else -1
+        # the tree starts after the branch to the masked variant, which begins right after g1
+        g0 = max(i for i in range(sts[0]) if opcode(ins[i][1]).startswith("BRA") and
+                 target(ins[i][1]) == ins[g1 + 1][0])
         cg = Counter(opcode(s) for _, s in ins[g0 + 1:g1 + 1])
         arr = [i for i, (_, s) in enumerate(ins) if opcode(s).startswith("SYNCS.ARRIVE") and i > g1]
         cr, nslots = Counter(), 0
