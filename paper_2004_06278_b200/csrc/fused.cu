@@ -344,11 +344,16 @@ static_assert(kWsThreads <= 1024, "one CTA of at most 32 warps");
 constexpr int kWsPer = kWsGen / kWsRed;                 // generator warps per reducer warp
 constexpr int kWsDepth = SQ_WS_DEPTH;                   // ring slots per generator warp
 constexpr int kWsEpochSteps = SQ_WS_EPOCH_STEPS;        // reducer steps (kWsPer slots each) per epoch
-// Two carry-save trees per generator iteration, folded by one more level into a weight-32 word
-// (one plane ripple per 64 samples instead of per 32): 1115 -> 1135 Gsamples/s.
+// SQ_WS_TREES carry-save trees per generator iteration, folded by more levels into one word
+// (one plane ripple per 32*SQ_WS_TREES samples instead of per 32): 1 tree 1115, 2 trees 1135,
+// 4 trees 1145 (adopted), 8 trees 1150 Gsamples/s with twice the code.
 #ifndef SQ_WS_TREE2
 #define SQ_WS_TREE2 1
 #endif
+#ifndef SQ_WS_TREES
+#define SQ_WS_TREES 4
+#endif
+static_assert(SQ_WS_TREES == 2 || SQ_WS_TREES == 4 || SQ_WS_TREES == 8, "2, 4 or 8 trees per generator iteration");
 #ifndef SQ_WS_SLOT_BATCHES
 #define SQ_WS_SLOT_BATCHES 4
 #endif
@@ -575,13 +580,16 @@ fused_ws_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64
     for (int p = 0; p < kPlanes; p++) pl[p] = 0;
     int since_flush = 0;
 #if SQ_WS_TREE2
-    // two 32-sample trees per iteration, their weight-16 words folded into a weight-32 word by
-    // one more carry-save level: one ripple into the planes per 64 samples
-    uint32_t sx = 0;   // weight-16 carry-save state
-    for (uint32_t b = 0; b < nb; b += 8) {
-      uint32_t s16[2];
+    // SQ_WS_TREES (2 or 4) 32-sample trees per iteration, their weight-16 words folded by more
+    // carry-save levels into one weight-16*SQ_WS_TREES word: one ripple into the count planes
+    // per 32*SQ_WS_TREES samples instead of per 32
+    constexpr int kTr = SQ_WS_TREES;
+    constexpr uint32_t kW = 16u * kTr;   // weight of the rippled word
+    uint32_t sx = 0, sx2 = 0, sx3 = 0;   // weight-16, -32 and -64 carry-save states
+    for (uint32_t b = 0; b < nb; b += 4 * kTr) {
+      uint32_t s16[kTr];
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
+      for (int h = 0; h < kTr; h++) {
         const uint32_t bb = b + 4 * h;
         if (bb + 4 <= nfull) {
           s16[h] = ws_gen_tree<false, STRIDED, BITREV>(st, wc, one, ring_g, full_g, empty_g, bb, 32, lane, ones,
@@ -592,8 +600,23 @@ fused_ws_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64
                                                       twos, fours, eights SQ_RING_TAG_PASS(tags + gw * kWsDepth));
         }
       }
+      // carry-save levels: weight 16 -> 32 (state sx) -> 64 (sx2) -> 128 (sx3)
       uint32_t c;
-      csa(c, sx, sx, s16[0], s16[1]);
+      if (kTr == 2) {
+        csa(c, sx, sx, s16[0], s16[1]);
+      } else if (kTr == 4) {
+        uint32_t c32a, c32b;
+        csa(c32a, sx, sx, s16[0], s16[1]);
+        csa(c32b, sx, sx, s16[2 % kTr], s16[3 % kTr]);
+        csa(c, sx2, sx2, c32a, c32b);
+      } else {
+        uint32_t c32[4], c64[2];
+#pragma unroll
+        for (int i = 0; i < 4; i++) csa(c32[i], sx, sx, s16[(2 * i) % kTr], s16[(2 * i + 1) % kTr]);
+        csa(c64[0], sx2, sx2, c32[0], c32[1]);
+        csa(c64[1], sx2, sx2, c32[2], c32[3]);
+        csa(c, sx3, sx3, c64[0], c64[1]);
+      }
 #pragma unroll
       for (int p = 0; p < kPlanes; p++) {
         const uint32_t tt = pl[p] & c;
@@ -604,14 +627,16 @@ fused_ws_kernel(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_t q, uint64
         since_flush = 0;
         uint32_t colcnt[16] = {};
 #pragma unroll
-        for (int p = 0; p < kPlanes; p++) { columns_add(colcnt, pl[p], 32u << p); pl[p] = 0; }
+        for (int p = 0; p < kPlanes; p++) { columns_add(colcnt, pl[p], kW << p); pl[p] = 0; }
         warp_flush16(colcnt, lo_cnt);
       }
     }
     uint32_t colcnt[16] = {};
     columns_add(colcnt, sx, 16);
+    columns_add(colcnt, sx2, 32);
+    columns_add(colcnt, sx3, 64);
 #pragma unroll
-    for (int p = 0; p < kPlanes; p++) { columns_add(colcnt, pl[p], 32u << p); pl[p] = 0; }
+    for (int p = 0; p < kPlanes; p++) { columns_add(colcnt, pl[p], kW << p); pl[p] = 0; }
 #else
     for (uint32_t b = 0; b < nb; b += 4) {
       uint32_t sixteens;
@@ -720,7 +745,8 @@ static int launch_fused_ws(uint64_t key, uint64_t ctr0, uint64_t stride, uint64_
   const uint64_t q = n / T, r = n % T;
   const uint64_t per = q + (r ? 1 : 0);
   // batches per lane, whole 4-batch trees (pairs of trees with SQ_WS_TREE2)
-  const uint64_t nb = SQ_WS_TREE2 ? ((per + 63) / 64) * 8 : ((per + 31) / 32) * 4;
+  const uint64_t nb = SQ_WS_TREE2 ? ((per + 32 * SQ_WS_TREES - 1) / (32 * SQ_WS_TREES)) * 4 * SQ_WS_TREES
+                                   : ((per + 31) / 32) * 4;
   if (nb > 0xFFFFFFF0ull) return SQ_ERANGE;
   const uint64_t nfull = q / 8;
   kern<<<(unsigned)blocks, kWsThreads, kWsSmem, stream>>>(key, ctr0, stride, q, r, (uint32_t)nb,
