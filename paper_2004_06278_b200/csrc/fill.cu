@@ -21,6 +21,16 @@
 
 namespace sq {
 
+// Unroll factor of the full-chunk loop, per output kind: 2 for the 64-bit kinds (store-bound:
+// c3 808.6 -> 827.2 Gsamples/s in burst A/B), 1 for the 32-bit kinds (unrolling by 2 or 4 costs
+// them 1-7 %).  SQ_FILL_UNROLL > 0 forces one factor for all kinds.
+#ifndef SQ_FILL_UNROLL
+#define SQ_FILL_UNROLL 0
+#endif
+template <int KIND>
+__host__ __device__ constexpr int fill_unroll() {
+  return SQ_FILL_UNROLL > 0 ? SQ_FILL_UNROLL : (kind_elem_bytes(KIND) == 8 ? 2 : 1);
+}
 #ifndef SQ_FILL_LANE_BYTES
 #define SQ_FILL_LANE_BYTES 64
 #endif
@@ -221,6 +231,7 @@ __global__ void __launch_bounds__(kFillThreads, KEYIMM ? kFillMinBlocksImm : kFi
         char* p = rowp + (int64_t)i0 * ES;
         i0 += nfull * J;
         cc += nfull;
+#pragma unroll fill_unroll<KIND>()
         for (; nfull; nfull--) {
           gen_lane<KIND, SPL, STRIDED, SQ_FILL_CHAIN2 && !KEYIMM>(s, rc, v, a.one);
 #ifdef SQ_FILL_NOSTORE   // experiment: generation without the output stream

@@ -19,7 +19,7 @@ ALU = ("IADD3", "LOP3", "SHF", "SEL", "ISETP", "MOV", "LEA", "PRMT", "VIADD", "I
 # kernel symbol substring, loop marker, samples per loop iteration, description
 LOOPS = [
     ("fill_kernelILi0ELb1ELb0E", "STG.E.ENL2.256", 16, "c2 u32 fill (key by value), per lane-chunk of 16"),
-    ("fill_kernelILi1ELb1ELb0E", "STG.E.ENL2.256", 8, "c3 u64 fill (key by value), per lane-chunk of 8"),
+    ("fill_kernelILi1ELb1ELb0E", "STG.E.ENL2.256", 16, "c3 u64 fill (key by value), per 2 lane-chunks of 8 (loop unrolled by 2)"),
     ("fill_kernelILi2ELb0ELb0E", "STG.E.ENL2.256", 16, "c4 f32 fill (device keys), per lane-chunk of 16"),
     ("fill_kernelILi0ELb0ELb0E", "STG.E.ENL2.256", 16, "c2 u32 fill (device keys), per lane-chunk of 16"),
 ]
@@ -70,7 +70,7 @@ def classify(c, samples):
 
 
 KEY_OF = {"c2 u32 fill (key by value), per lane-chunk of 16": "c2",
-          "c3 u64 fill (key by value), per lane-chunk of 8": "c3",
+          "c3 u64 fill (key by value), per 2 lane-chunks of 8 (loop unrolled by 2)": "c3",
           "c4 f32 fill (device keys), per lane-chunk of 16": "c4",
           "c2 u32 fill (device keys), per lane-chunk of 16": "c2_devkeys",
           "c5 fused statistics (warp-specialised), generator tree + reducer slot, per 32 samples": "c5",
@@ -145,8 +145,7 @@ def per_workload(lib: str = LIB) -> dict:
                       "fma_slots_per_sample": round(v["fma_slots_per_sample"], 4),
                       "multiply_instructions_per_sample": round(v["multiply_instructions_per_sample"], 4),
                       "alu_per_sample": round(v["alu_per_sample"], 4),
-                      "mix_per_sample": {op: round(c / (32 if k.startswith("c5") else
-                                                        (8 if k == "c3" else 16)), 4)
+                      "mix_per_sample": {op: round(c / (32 if k.startswith("c5") else 16), 4)
                                          for op, c in v["mix"].items()},
                       "loop": desc, "symbol": v["symbol"]}
     return res
