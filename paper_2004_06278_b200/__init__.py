@@ -333,6 +333,7 @@ def _zeros(shape, dev, stream):
     so that it is ordered before the accumulating kernel even when `stream` is not current."""
     if stream is None:
         return torch.zeros(shape, dtype=torch.int64, device=dev)
+    _stream_handle(stream, dev)   # a stream of another device is rejected here already
     with torch.cuda.stream(stream):
         return torch.zeros(shape, dtype=torch.int64, device=dev)
 
