@@ -595,10 +595,14 @@ def main():
                                           ("c4", "c4", 20, "auto"), ("c5", "c5", 3, "auto")):
             a2.steps, a2.warmup = steps, 3
             ww = SI.CONFIGS[wname]
+            # the same starting point for every secondary line: 2 s idle, so that one config's
+            # power draw does not carry into the next one's short measurement
+            torch.cuda.synchronize(local)
+            time.sleep(2.0)
             r = run_ours(a2, ww, rank, world, local, entry=entry)
             rl = roofline_for(ww, r, peaks, peaks_src, prof, sass, name)
             extra[name] = {"value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"], "steps": steps,
-                           "roofline": rl, "clocks": r["clocks"], "gpu_launches": steps}
+                           "roofline": rl, "clocks": r["clocks"], "gpu_launches": steps, "idle_before_s": 2.0}
             if name == "c2_devkeys":
                 extra[name]["entry"] = "sq_fill_u32 (device key array, SURVEY.md 8(b))"
             if "allreduce_ms" in r:
