@@ -58,6 +58,20 @@ __device__ __forceinline__ uint32_t scaled_from(uint32_t y, uint32_t z, uint32_t
   return (((x * x + z) & mask) >> h) << 16;   // round 4
 }
 
+// Histogram update with the increment (v & 0x10000) | one as ONE LOP3 (`one` is the opaque
+// kernel argument; with two immediates ptxas needs two instructions).  SQ_SCALED_INC2 keeps
+// hist16.cuh's predicate + select form.
+__device__ __forceinline__ uint32_t scaled_hist_add(uint32_t* bins, uint32_t v, uint32_t one, bool valid = true) {
+#ifdef SQ_SCALED_INC2
+  return hist_add_sweep(bins, v, one, valid);
+#else
+  uint32_t inc;
+  asm("lop3.b32 %0, %1, 0x10000, %2, 0xEA;" : "=r"(inc) : "r"(v), "r"(one));   // (a & b) | c
+  if (!valid) inc = 0;
+  return atomicAdd(&bins[v >> 17], inc);
+#endif
+}
+
 // All words -> the key's global histogram row, zeroed (A/B packing of hist16.cuh).
 __device__ __noinline__ void flush_scaled(uint32_t* bins, uint32_t nwords, uint32_t nbins,
                                           unsigned long long* hrow) {
@@ -100,14 +114,14 @@ __global__ void __launch_bounds__(kScaledThreads, 1) scaled_hist_kernel(ScaledAr
 #pragma unroll 8
       for (int i = 0; i < kScaledEpoch; i++) {
         const uint32_t z = W32 ? y + key : (y + key) & a.mask;
-        acc |= hist_add_sweep(bins, scaled_from<W32>(y, z, a.h, a.mask), a.one);
+        acc |= scaled_hist_add(bins, scaled_from<W32>(y, z, a.h, a.mask), a.one);
         y = z;
       }
     } else {
 #pragma unroll 4
       for (int i = 0; i < kScaledEpoch; i++) {
         const uint32_t z = W32 ? y + key : (y + key) & a.mask;
-        acc |= hist_add_sweep(bins, scaled_from<W32>(y, z, a.h, a.mask), a.one, done + i < cnt);
+        acc |= scaled_hist_add(bins, scaled_from<W32>(y, z, a.h, a.mask), a.one, done + i < cnt);
         y = z;
       }
     }
