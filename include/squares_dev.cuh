@@ -78,6 +78,8 @@ __device__ __forceinline__ uint64_t add64_3(uint64_t a, uint64_t b, uint64_t c) 
 //   3  IMAD(xl, SHF(RZ:xh, 1), hi)           -- the doubling as a funnel shift with an immediate
 //                                               amount: ALU pipe, one register read
 //   6  hi + ((xl * xh) << 1)                 -- product first, doubling and add after it (LEA)
+//   +8 (round_rot only) the square's 64-bit addend added through an explicit carry chain (see
+//      round_rot): removes the VIADD copy ptxas otherwise puts after every IMAD.WIDE.U32
 // Measured on B200: form 3 is fastest for the library's 32-bit fills (the ALU has room next to
 // the stores), form 0 for compute-only loops (fused statistics, Stream): the default here.
 #ifndef SQ_ROUND_FORM
@@ -113,6 +115,21 @@ __device__ __forceinline__ uint32_t cross_add(uint32_t xl, uint32_t xh, uint32_t
 // x <- rot32(x*x + w), x held as (xh, xl).  P:24-26.
 template <int FORM = SQ_ROUND_FORM>
 __device__ __forceinline__ void round_rot(uint32_t& xh, uint32_t& xl, uint64_t w, uint32_t one = 1) {
+  if (FORM & 8) {
+    // +8: the 64-bit sum xl*xl + w written as a 32-bit product pair and an explicit add.cc /
+    // addc carry chain (PTX), the cross term then in form FORM & 7.  ptxas still emits ONE
+    // IMAD.WIDE.U32 with the addend folded in, but no longer inserts the VIADD copy of its high
+    // register before the cross-term instruction (measured: u32 fill 15.25 -> 14.06 SASS
+    // instructions per sample, c2 +5 %, c4 +6 %).
+    uint32_t plo, phi, tlo, thi;
+    asm("mul.lo.u32 %0, %2, %2;\n\tmul.hi.u32 %1, %2, %2;" : "=r"(plo), "=r"(phi) : "r"(xl));
+    asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;"
+        : "=r"(tlo), "=r"(thi) : "r"(plo), "r"(phi), "r"(lo32(w)), "r"(hi32(w)));
+    const uint32_t hi = cross_add<(FORM & 7)>(xl, xh, thi, one);
+    xh = tlo;
+    xl = hi;
+    return;
+  }
   uint64_t t = mad_wide(xl, xl, w);
   uint32_t hi = cross_add<FORM>(xl, xh, hi32(t), one);
   xh = lo32(t);

@@ -79,9 +79,9 @@ __device__ __forceinline__ RowConst<SPL> row_const(uint64_t key, uint64_t stride
 }
 
 // Output words of one sample j of kind KIND into v (little-endian 64-bit elements).
-// Cross-term form (squares_dev.cuh cross_add) per output kind, measured on B200
-// (DESIGN.md 7.5): the funnel-shift doubling (3) for the 32-bit kinds (u32, f32), the plain
-// form (0) for the squares64 kinds (store-bound).
+// Cross-term form (squares_dev.cuh cross_add): the squares64 kinds (store-bound) use the plain
+// form 0 in every round (fill_form); the 32-bit kinds use a form per round (SQ_FILL_MIX*,
+// below).  SQ_FILL_FORM >= 0 forces one form for every kind and round (experiments).
 #ifndef SQ_FILL_FORM
 #define SQ_FILL_FORM -1
 #endif
@@ -90,16 +90,24 @@ __device__ __forceinline__ RowConst<SPL> row_const(uint64_t key, uint64_t stride
 #endif
 template <int KIND>
 __host__ __device__ constexpr int fill_form() {
-  return SQ_FILL_FORM >= 0 ? SQ_FILL_FORM : ((KIND == KIND_U32 || KIND == KIND_F32) ? 3 : 0);
+  return SQ_FILL_FORM >= 0 ? SQ_FILL_FORM : 0;
 }
+// Cross-term forms per round for the 32-bit kinds (include/squares_dev.cuh cross_add): rounds 2
+// and 3 as form 11 (= 8 + 3: the square's addend through an explicit carry chain, which drops
+// ptxas' VIADD copy after each IMAD.WIDE, and the funnel-shift doubling), round 4 as form 3.
+// Burst A/B on B200 (c2 by value / c2 device keys / c4): 11/11/3 1460 / 1379 /
+// 1344 vs 3/3/3 1392 / 1353 / 1266; 11/3/3 1461 / 1354 / 1333; 8/8/3 1403 / 1339 / 1298;
+// 9/9/3 1357 / 1378 / 1295; 11/11/0 1399 / 1340 / 1302.
+#ifndef SQ_FILL_MIX2
+#define SQ_FILL_MIX2 11
+#define SQ_FILL_MIX3 11
+#define SQ_FILL_MIX4 3
+#endif
 template <int KIND, int FORM, int NW>
 __device__ __forceinline__ void put(uint32_t (&v)[NW], int j, uint64_t y, uint64_t z, uint64_t u, uint32_t one) {
   if (KIND == KIND_U32 || KIND == KIND_F32) {
-#ifdef SQ_FILL_MIX2
-    const uint32_t o = squares32_mix<SQ_FILL_MIX2, SQ_FILL_MIX3, SQ_FILL_MIX4>(y, z, u, one);
-#else
-    const uint32_t o = squares32_from<FORM>(y, z, u, one);
-#endif
+    const uint32_t o = (SQ_FILL_FORM >= 0) ? squares32_from<(SQ_FILL_FORM >= 0 ? SQ_FILL_FORM : 0)>(y, z, u, one)
+                                           : squares32_mix<SQ_FILL_MIX2, SQ_FILL_MIX3, SQ_FILL_MIX4>(y, z, u, one);
     // f32: the exact integer float(u >> 8) here; the 2^-24 scale is applied to pairs of lanes'
     // words afterwards with one packed FMUL2 (scale_f32_pairs), exact as before
     v[j] = (KIND == KIND_F32) ? (SQ_FILL_FMUL2 ? __float_as_uint(__uint2float_rn(o >> 8))
