@@ -139,8 +139,8 @@ __device__ __forceinline__ void round_rot(uint32_t& xh, uint32_t& xl, uint64_t w
 // High 32 bits of x*x + w (the final extraction of P:27 and P:63).
 template <int FORM = SQ_ROUND_FORM>
 __device__ __forceinline__ uint32_t round_hi(uint32_t xh, uint32_t xl, uint64_t w, uint32_t one = 1) {
-  uint64_t t = mad_wide(xl, xl, w);
-  return cross_add<FORM>(xl, xh, hi32(t), one);
+  uint64_t t = mad_wide(xl, xl, w);   // IMAD.HI: its result needs no copy, so the +8 bit is moot
+  return cross_add<(FORM & 7)>(xl, xh, hi32(t), one);
 }
 
 // squares32 given y = ctr*key, z = y + key and u = y*y + y (round 1's sum).  P:21-28.
@@ -240,6 +240,15 @@ __device__ __forceinline__ uint64_t squares64(uint64_t ctr, uint64_t key) {
   return squares64_from(y, y + key, y * y + y);
 }
 
+// Cross-term forms per round of Stream::next_u32 (rounds 2, 3, 4): the carry-chain addend with
+// the product-first cross term in rounds 2-3 (14 = 8 + 6), form 6 in round 4.  Measured on
+// B200 (XOR-folded draws, 303104 threads x 4096): 14/14/6 1327 Gsamples/s, 14/14/2 1326,
+// 0/0/0 1256, 14/14/0 1253, 11/11/3 1240, 14/14/3 1234.
+#ifndef SQ_STREAM_MIX2
+#define SQ_STREAM_MIX2 14
+#define SQ_STREAM_MIX3 14
+#define SQ_STREAM_MIX4 6
+#endif
 // A per-thread stream over consecutive counters ctr, ctr+1, ... of one key (the batch of
 // n sequential draws equal the batch evaluation).  Each draw costs the round
 // multiplies only; the counter walk is the Weyl/finite-difference step.  Counters wrap mod
@@ -251,7 +260,7 @@ class Stream {
   }
   __device__ __forceinline__ uint32_t next_u32() {
     const uint64_t z = add64(s_.y, key_);
-    const uint32_t o = squares32_from(s_.y, z, s_.u);
+    const uint32_t o = squares32_mix<SQ_STREAM_MIX2, SQ_STREAM_MIX3, SQ_STREAM_MIX4>(s_.y, z, s_.u);
     advance();
     return o;
   }
