@@ -535,8 +535,6 @@ def _pipes(prof, name, kname):
     return {"pipes_ncu": {"fmaheavy_pct": p.get("fmaheavy_pct"), "alu_pct": p.get("alu_pct"),
                           "issue_pct": p.get("issue_active_pct"),
                           "inst_executed_per_sample": p.get("inst_executed_per_sample"),
-                          "fmaheavy_inst_per_sample": p.get("inst_fmaheavy_per_sample"),
-                          "alu_inst_per_sample": p.get("inst_alu_per_sample"),
                           "source": "profiles/ncu_summary.json (ncu --set full, same kernel)"}}
 
 

@@ -32,9 +32,6 @@ KEYS = {
     "smem_atom_bank_conflicts": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum",
     "inst_executed": "smsp__inst_executed.sum",
     "sm_clock_hz": "sm__cycles_elapsed.avg.per_second",
-    "inst_fmaheavy": "smsp__inst_executed_pipe_fmaheavy.sum",
-    "inst_alu": "smsp__inst_executed_pipe_alu.sum",
-    "inst_lsu": "smsp__inst_executed_pipe_lsu.sum",
 }
 UNIT_SCALE = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1, "usecond": 1e3, "msecond": 1e6,
               "nsecond": 1, "ns": 1, "us": 1e3, "ms": 1e6, "GHz": 1e9, "MHz": 1e6, "Hz": 1, "hz": 1}
@@ -89,7 +86,7 @@ def main():
         # executed instructions per output sample (warp instructions x 32 / samples of the launch;
         # tools/profile_all.sh launches c2 2^30, c3 2^29, c4 2^30, c5 2^34 samples)
         ns = {"c2": 1 << 30, "c3": 1 << 29, "c4": 1 << 30, "c5": 1 << 34}[cfg]
-        for k in ("inst_executed", "inst_fmaheavy", "inst_alu", "inst_lsu"):
+        for k in ("inst_executed",):
             if isinstance(s.get(k), float):
                 s[k + "_per_sample"] = s[k] * 32 / ns
         summary[cfg] = s
