@@ -77,3 +77,22 @@ def test_roofline_fields():
             assert rl["algorithmic_bytes_per_launch"] == w.nkeys * w.n * w.elem_bytes
         else:
             assert rl["bound"] == "alu" and rl["traffic"] is None
+
+
+def test_sass_counts_cover_every_bench_line():
+    """The SASS-per-sample counts bench.py embeds in each roofline (tools/sass_counts.py,
+    cuobjdump, no GPU) find every hot loop of the built library, with plausible totals."""
+    import shutil
+    import pytest
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    import __graft_entry__
+    __graft_entry__.build()
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import sass_counts
+    d = sass_counts.per_workload()
+    assert {"c2", "c2_devkeys", "c3", "c4", "c5"} <= set(d)
+    for k, v in d.items():
+        assert 8 <= v["instructions_per_sample"] <= 40, (k, v["instructions_per_sample"])
+        assert v["mix_per_sample"].get("IMAD.WIDE.U32", 0) >= 1, k
+    assert d["c5"]["mix_per_sample"].get("ATOMS.ADD") == 1.0
