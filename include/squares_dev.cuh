@@ -169,10 +169,11 @@ __device__ __forceinline__ uint64_t squares64_from(uint64_t y, uint64_t z, uint6
   uint32_t xh = lo32(u), xl = hi32(u);
   round_rot<FORM>(xh, xl, z, one);      // round 2
   round_rot<FORM>(xh, xl, y, one);      // round 3
-  uint64_t t = mad_wide(xl, xl, z);     // round 4 (full 64-bit sum)
-  uint32_t th = cross_add<FORM>(xl, xh, hi32(t), one);
-  uint32_t tl = lo32(t);
-  uint32_t r5 = round_hi<FORM>(tl, th, y, one);  // round 5 on rot32(t) = (tl, th)
+  // round 4 (full 64-bit sum): round_rot without the rotation -- after it (xh, xl) holds
+  // (lo, hi) of t, i.e. rot32(t), which is exactly round 5's input
+  round_rot<FORM>(xh, xl, z, one);
+  const uint32_t tl = xh, th = xl;
+  const uint32_t r5 = round_hi<FORM>(tl, th, y, one);  // round 5 on rot32(t) = (tl, th)
   return ((uint64_t)th << 32) | (uint64_t)(tl ^ r5);
 }
 

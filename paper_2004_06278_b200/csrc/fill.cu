@@ -85,12 +85,15 @@ __device__ __forceinline__ RowConst<SPL> row_const(uint64_t key, uint64_t stride
 #ifndef SQ_FILL_FORM
 #define SQ_FILL_FORM -1
 #endif
+#ifndef SQ_FILL64_FORM
+#define SQ_FILL64_FORM 0   // cross-term form of the squares64 kinds (all rounds)
+#endif
 #ifndef SQ_FILL_FMUL2
 #define SQ_FILL_FMUL2 1   // f32 scale as a packed FMUL2 over word pairs (gen_lane)
 #endif
 template <int KIND>
 __host__ __device__ constexpr int fill_form() {
-  return SQ_FILL_FORM >= 0 ? SQ_FILL_FORM : 0;
+  return SQ_FILL_FORM >= 0 ? SQ_FILL_FORM : SQ_FILL64_FORM;
 }
 // Cross-term forms per round for the 32-bit kinds (include/squares_dev.cuh cross_add): rounds 2
 // and 3 as form 11 (= 8 + 3: the square's addend through an explicit carry chain, which drops
