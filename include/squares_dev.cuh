@@ -31,7 +31,7 @@
 // Per squares32 sample: rounds 2-4 = 2 IMAD.WIDE.U32 + 1 IMAD.HI.U32 + 3 IMAD (9 FMA-heavy
 // pipe slots: IMAD 64 lanes/clk/SM, WIDE/HI 2 slots each -- 24-27 lanes/clk/SM measured in
 // dependent loops on B200) plus 3 doublings and the two 64-bit walk adds.  squares64 adds
-// round 4's full sum and round 5.  A Stream draw runs at ~1.25 Tsamples/s per B200 when the
+// round 4's full sum and round 5.  A Stream draw runs at ~1.33 Tsamples/s per B200 when the
 // value is consumed in registers (tools/bench_next.py).
 #pragma once
 #include <stdint.h>
@@ -80,8 +80,9 @@ __device__ __forceinline__ uint64_t add64_3(uint64_t a, uint64_t b, uint64_t c) 
 //   6  hi + ((xl * xh) << 1)                 -- product first, doubling and add after it (LEA)
 //   +8 (round_rot only) the square's 64-bit addend added through an explicit carry chain (see
 //      round_rot): removes the VIADD copy ptxas otherwise puts after every IMAD.WIDE.U32
-// Measured on B200: form 3 is fastest for the library's 32-bit fills (the ALU has room next to
-// the stores), form 0 for compute-only loops (fused statistics, Stream): the default here.
+// Measured on B200, per round 2 / 3 / 4: 11 / 11 / 3 for the library's 32-bit
+// fills, 14 / 14 / 3 for the fused statistics walk, 14 / 14 / 6 for Stream::next_u32; form 0
+// is the default of squares32_from / squares64_from.
 #ifndef SQ_ROUND_FORM
 #define SQ_ROUND_FORM 0
 #endif
